@@ -1,0 +1,177 @@
+/*
+ * nnp_b200.h -- C ABI of the B200-native neighbor search + TensorNet energy/forces step.
+ *
+ * This is the drop-in boundary for the hot path of the reference package `nnpkit`
+ * (/root/reference/pkg/src/nnpkit).  Every entry point cites the reference interface it
+ * replaces.  Conventions shared by all calls:
+ *
+ *  - plain pointers and sizes only; all array pointers are DEVICE pointers unless the
+ *    name ends in `_host`;
+ *  - the caller owns every buffer (inputs, outputs, workspace); nothing is allocated
+ *    inside a call, so every call is CUDA-graph capturable ("static shapes
+ *    and fixed memory addresses");
+ *  - calls only enqueue work on `stream` and never synchronise;
+ *  - return value 0 = success, negative = error code below; nnp_last_error() gives a
+ *    thread-local message.  No C++ exception crosses this boundary;
+ *  - data-dependent overflow is reported through device memory (`counts`), mirroring
+ *    CapacityError.required (errors.py:32-45, neighbors.py:204-207): kernels keep
+ *    counting past capacity (_neighbor_kernels.py:43-50) and the host wrapper raises.
+ */
+#ifndef NNP_B200_H
+#define NNP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *nnp_stream_t; /* a cudaStream_t */
+
+#define NNP_OK 0
+#define NNP_ERR_INVALID (-1)   /* bad argument (host-detectable ValidationError) */
+#define NNP_ERR_WORKSPACE (-2) /* workspace too small */
+#define NNP_ERR_CUDA (-3)      /* a CUDA runtime call failed */
+#define NNP_ERR_UNSUPPORTED (-4)
+
+/* box kinds: _neighbor_kernels.py:18-20 */
+#define NNP_BOX_NONE 0
+#define NNP_BOX_ORTHORHOMBIC 1
+#define NNP_BOX_TRICLINIC 2
+
+/* strategies after host-side resolution of "auto" (neighbors.py:155-157) */
+#define NNP_STRATEGY_BRUTE 0
+#define NNP_STRATEGY_CELL 1
+
+/* flags */
+#define NNP_NL_FULL_LIST 1  /* NeighborSpec.full_list (neighbors.py:43) */
+#define NNP_NL_SELF_LOOPS 2 /* NeighborSpec.include_self_loops (neighbors.py:42) */
+#define NNP_NL_RENUMBER 4   /* rows/cols in cell-sorted atom numbering (internal model path) */
+#define NNP_NL_F32_OUT 8    /* deltas/distances written as float32 instead of float64 */
+#define NNP_NL_NO_PAD 16    /* do not write -1/0 sentinels into the unused tail */
+
+const char *nnp_last_error(void);
+int nnp_version(void);
+
+/* ------------------------------------------------------------------ neighbor search
+ * Replaces build_neighbor_list (neighbors.py:136-235) and the four numba kernels
+ * (_neighbor_kernels.py:24-233), the grid construction (neighbors.py:103-124) and the cell
+ * sort (neighbors.py:127-133).
+ */
+typedef struct nnp_nl_params {
+    int32_t n_atoms;
+    int32_t n_samples;    /* max(batch)+1 */
+    int32_t capacity;     /* rows of the output arrays (NeighborSpec.capacity) */
+    int32_t box_kind;     /* NNP_BOX_* */
+    int32_t strategy;     /* NNP_STRATEGY_* */
+    int32_t flags;        /* NNP_NL_* */
+    int32_t grid_dims[3]; /* periodic cell grid floor(widths/cutoff), each >= 3 (host computed,
+                             neighbors.py:103-109); ignored for open systems (device computed) */
+    int32_t max_cells;    /* cells the workspace is sized for (open systems clamp to it) */
+    double cutoff_lower, cutoff_upper;
+    double box[9];        /* rows a,b,c, lower triangular (system.py:34-38) */
+    double inv_box[9];    /* inverse of box (host computed, float64) */
+} nnp_nl_params;
+
+int nnp_nl_workspace_bytes(const nnp_nl_params *p, size_t *bytes);
+
+/*
+ * Outputs:
+ *   pairs  [capacity,2] int32   (i, j); -1 in unused rows unless NNP_NL_NO_PAD
+ *   deltas [capacity,3] float64 (float32 with NNP_NL_F32_OUT)  r_i - r_j, minimum image
+ *   dists  [capacity]   same type
+ *   row_ptr [n_atoms+1] int32 or NULL: CSR offsets of the (i, j)-sorted rows
+ *   order   [n_atoms]   int32 or NULL: with NNP_NL_RENUMBER, order[s] = original index of
+ *                                      the atom numbered s in the output (identity otherwise)
+ *   counts  int32[4]: [0] rows required (directed pairs + loops; may exceed capacity, then
+ *                     nothing is written), [1] longest row, [2] number of cells, [3] reserved
+ * Rows come out sorted by (i, j) -- the reference's deterministic order (neighbors.py:221-225).
+ * `pos` is float64 [n,3]; `batch` int32 [n], non-decreasing from 0 (system.py:231-235).
+ */
+int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int32_t *batch, int32_t *pairs,
+                 void *deltas, void *dists, int32_t *row_ptr, int32_t *order, int32_t *counts,
+                 void *workspace, size_t workspace_bytes, nnp_stream_t stream);
+
+/* float32 positions -> float64 (exact), so the model path tests the same bits as the oracle */
+int nnp_f32_to_f64(const float *src, double *dst, int64_t n, nnp_stream_t stream);
+
+/*
+ * distance_pullback (neighbors.py:345-355): grad[i] += g_e * u_e, grad[j] -= g_e * u_e over
+ * valid rows; self loops contribute nothing.  deltas/dists/g/grad are float64.  flag_out[0]
+ * is 0x7f7f7f7f when all is well, else 1 + the first row holding a zero-distance non-loop pair
+ * (NumericError, neighbors.py:333-338).
+ */
+int nnp_distance_pullback(const int32_t *pairs, const double *deltas, const double *dists,
+                          const double *g, int32_t count, int32_t n_atoms, double *grad,
+                          int32_t *flag_out, nnp_stream_t stream);
+
+/* ------------------------------------------------------------------ TensorNet step
+ * Replaces GraphPotential.evaluate (graphnet.py:567-580) = forward (graphnet.py:317-412) +
+ * backward_forces (graphnet.py:516-537) with the TensorNet arithmetic of SURVEY.md
+ * Appendix A.  Weights are float32 device arrays prepared by the host wrapper.
+ */
+#define NNP_TN_MAX_LAYERS 8
+
+typedef struct nnp_tn_model {
+    int32_t channels;  /* C: 32, 64 or 128 (GNConfig.embedding_dimension, graphnet.py:59) */
+    int32_t num_rbf;   /* K (only used by the host when it builds the tables) */
+    int32_t num_layers;
+    int32_t max_z;
+    int32_t num_knots; /* radial tables: cubic Hermite in u = exp(cutoff_lower - d) */
+    float cutoff_lower, cutoff_upper;
+    float u_min, u_step; /* knot k sits at u_min + k*u_step */
+    float mean, std;     /* per-atom raw*std + mean (graphnet.py:406) */
+    float h2_b;
+    /* species tables: Z_e = z_recv[z_i] + z_send[z_j]  (emb2 bias folded into z_send) */
+    const float *z_recv; /* [max_z, C] */
+    const float *z_send; /* [max_z, C] */
+    /* radial tables [(L+1)][num_knots][2][3][C]: table 0 = distance projections dp1..3 of the
+       embedding, table 1+l = radial MLP of layer l (before the cosine envelope);
+       [..][0] = value, [..][1] = u_step * d(value)/du */
+    const float *tables;
+    const float *init_norm_g, *init_norm_b;             /* [C] */
+    const float *es0_w, *es0_wT, *es0_b;                /* [2C,C], [C,2C], [2C] */
+    const float *es1_w, *es1_wT, *es1_b;                /* [3C,2C], [2C,3C], [3C] */
+    const float *et_w, *et_wT;                          /* [3,C,C] each */
+    const float *layer_t_w[NNP_TN_MAX_LAYERS];          /* [6,C,C] */
+    const float *layer_t_wT[NNP_TN_MAX_LAYERS];         /* [6,C,C] transposed */
+    const float *out_norm_g, *out_norm_b;               /* [3C] */
+    const float *lin_w, *lin_wT, *lin_b;                /* [C,3C], [3C,C], [C] */
+    const float *h1_w, *h1_wT, *h1_b;                   /* [C/2,C], [C,C/2], [C/2] */
+    const float *h2_w;                                  /* [C/2] */
+} nnp_tn_model;
+
+int nnp_tn_workspace_bytes(const nnp_tn_model *m, int32_t n_atoms, int32_t capacity,
+                           int32_t n_samples, size_t *bytes);
+
+/*
+ * One energy-and-forces evaluation on a prebuilt directed neighbor structure in CSR form
+ * (full list with self loops, rows sorted by (i, j), as nnp_nl_build emits with
+ * NNP_NL_FULL_LIST | NNP_NL_SELF_LOOPS | NNP_NL_F32_OUT).
+ *   species [n] int32, batch [n] int32: in ORIGINAL atom order
+ *   order   [n] int32 or NULL: atom numbering of the neighbor structure (see nnp_nl_build)
+ *   row_ptr [n+1], pairs [capacity,2] int32, deltas [capacity,3] f32, dists [capacity] f32
+ *   energy [n_samples] f32, forces [n,3] f32 (or NULL: energy only), per_atom [n] f32 or NULL;
+ *   all three in original atom order.
+ *   nl_counts: the int32[4] written by nnp_nl_build; if counts[0] > capacity the step writes
+ *   nothing (the host raises CapacityError after the stream has drained).
+ */
+int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_samples,
+                         int32_t capacity, const int32_t *species, const int32_t *batch,
+                         const int32_t *order, const int32_t *row_ptr, const int32_t *pairs,
+                         const float *deltas, const float *dists, const int32_t *nl_counts,
+                         float *energy, float *forces, float *per_atom, void *workspace,
+                         size_t workspace_bytes, nnp_stream_t stream);
+
+/* Test hook: out[M,N] = A[M,K] * W[N,K]^T (+ bias[N]) through the same tile engine the node
+ * kernels use (3xTF32 tensor-core path or FP32 FFMA). */
+int nnp_test_gemm_nt(const float *A, const float *W, const float *bias, float *out, int32_t M,
+                     int32_t N, int32_t K, nnp_stream_t stream);
+/* Test hook: 1 = 3xTF32 tensor-core inner loop (default), 0 = FP32 FFMA inner loop. */
+int nnp_set_gemm_mode(int use_mma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNP_B200_H */

@@ -347,9 +347,11 @@ def radial_mlp_dd(params, l, rho, drho_dd, cache):
 
 def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, deltas, dists,
                           n_samples: Optional[int] = None, want_forces: bool = True,
-                          return_intermediates: bool = False):
+                          return_intermediates: bool = False, edge_chunk: int = 32768):
     """Same function as energy_forces_torch in irreducible components, with the reverse
-    sweep written out by hand.  ``dists`` must equal |deltas| (0 on loops)."""
+    sweep written out by hand.  ``dists`` must equal |deltas| (0 on loops).  Edge-level
+    temporaries are produced ``edge_chunk`` edges at a time (and the radial MLP recomputed in
+    the reverse sweep) so that systems with millions of edges fit in host memory."""
     C, K, L = cfg.embedding_dimension, cfg.num_rbf, cfg.num_layers
     P = params
     z = np.asarray(species, dtype=np.int64)
@@ -368,19 +370,35 @@ def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, delt
     rl, ru = cfg.cutoff_lower, cfg.cutoff_upper
     phi = cosine_cutoff(d, rl, ru)
     dphi = cosine_cutoff_grad(d, rl, ru)
-    rho = rbf_expnorm(d, P["rbf_means"], P["rbf_betas"], rl)
-    drho = rbf_expnorm_dd(d, P["rbf_means"], P["rbf_betas"], rl)
     basis = edge_basis(u, loop)                                   # [E,9]
+    chunks = [slice(s, min(s + edge_chunk, E)) for s in range(0, E, edge_chunk)]
+    gI = GROUP == 0
+    gA = GROUP == 1
+    gS = GROUP == 2
+
+    def rho_of(sl):
+        return (rbf_expnorm(d[sl], P["rbf_means"], P["rbf_betas"], rl),
+                rbf_expnorm_dd(d[sl], P["rbf_means"], P["rbf_betas"], rl))
 
     # ------------------------------------------------------------------ forward
     Wa, Wb = P["emb2_w"][:, :C], P["emb2_w"][:, C:]
     Zt_r = P["emb"] @ Wa.T                                         # hoisted tables [max_z, C]
     Zt_s = P["emb"] @ Wb.T
-    Z = Zt_r[z[recv]] + Zt_s[z[send]] + P["emb2_b"]                # [E,C]
-    dpv = np.stack([rho @ P["dp_w"][k].T + P["dp_b"][k] for k in range(3)], axis=-1)  # [E,C,3]
-    w = dpv * (phi[:, None] * Z)[:, :, None]                       # [E,C,3]
-    contrib = w[:, :, GROUP] * basis[:, None, :]                   # [E,C,9]
-    X0 = segment_sum(contrib.reshape(E, C * 9), recv, N).reshape(N, C, 9)
+
+    def embed_weights(sl):
+        rho, drho = rho_of(sl)
+        Z = Zt_r[z[recv[sl]]] + Zt_s[z[send[sl]]] + P["emb2_b"]              # [e,C]
+        dpv = np.stack([rho @ P["dp_w"][k].T + P["dp_b"][k] for k in range(3)], axis=-1)
+        ddp = np.stack([drho @ P["dp_w"][k].T for k in range(3)], axis=-1)
+        return Z, dpv, ddp
+
+    X0 = np.zeros((N, C * 9))
+    for sl in chunks:
+        Z, dpv, _ = embed_weights(sl)
+        w = dpv * (phi[sl, None] * Z)[:, :, None]                            # [e,C,3]
+        contrib = w[:, :, GROUP] * basis[sl, None, :]
+        X0 += segment_sum(contrib.reshape(-1, C * 9), recv[sl], N)
+    X0 = X0.reshape(N, C, 9)
     n0 = frob(X0, X0)                                              # [N,C]
     ln0, ln0_cache = _ln_fwd(n0, P["init_norm_g"], P["init_norm_b"])
     e0 = ln0 @ P["es0_w"].T + P["es0_b"]
@@ -391,14 +409,17 @@ def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, delt
 
     saved = []
     for l in range(L):
-        ft, mlp_cache = radial_mlp(P, l, rho)                      # [E,3C]
-        f = (ft * phi[:, None]).reshape(E, C, 3)
         nx = frob(X, X) + 1.0
         Xh = X / nx[:, :, None]
         T = P[f"l{l}_t_w"]
         Yc = mix3(T[:3], Xh)                                       # I',A',S' components
-        msg = f[:, :, GROUP] * Yc[send]
-        Mc = segment_sum(msg.reshape(E, C * 9), recv, N).reshape(N, C, 9)
+        Mc = np.zeros((N, C * 9))
+        for sl in chunks:
+            ft, _ = radial_mlp(P, l, rho_of(sl)[0])
+            f = (ft * phi[sl, None]).reshape(-1, C, 3)
+            msg = f[:, :, GROUP] * Yc[send[sl]]
+            Mc += segment_sum(msg.reshape(-1, C * 9), recv[sl], N)
+        Mc = Mc.reshape(N, C, 9)
         Mf, Yf = to_full(Mc), to_full(Yc)
         Pf = Mf @ Yf + Yf @ Mf
         Pc = from_full(Pf)
@@ -407,13 +428,9 @@ def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, delt
         Dc = mix3(T[3:], Qc)
         Df = to_full(Dc)
         Xn = Xh + Dc + from_full(Df @ Df)
-        saved.append(dict(X=X, nx=nx, Xh=Xh, Yc=Yc, Mc=Mc, Pc=Pc, npn=npn, Dc=Dc, ft=ft,
-                          mlp_cache=mlp_cache))
+        saved.append(dict(X=X, nx=nx, Xh=Xh, Yc=Yc, Mc=Mc, Pc=Pc, npn=npn, Dc=Dc))
         X = Xn
 
-    gI = GROUP == 0
-    gA = GROUP == 1
-    gS = GROUP == 2
     XI, XA, XS = X * gI, X * gA, X * gS
     feats = np.concatenate([dot_I(XI, XI), dot_A(XA, XA), dot_S(XS, XS)], axis=-1)  # [N,3C]
     lnr, lnr_cache = _ln_fwd(feats, P["out_norm_g"], P["out_norm_b"])
@@ -452,13 +469,18 @@ def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, delt
         G_M = from_full(GPf @ np.swapaxes(Yf, -1, -2) + np.swapaxes(Yf, -1, -2) @ GPf)
         G_Y = from_full(np.swapaxes(Mf, -1, -2) @ GPf + GPf @ np.swapaxes(Mf, -1, -2))
         # edge op  M_i = sum_e f_e[:,grp] * Yc_j
-        f = (sv["ft"] * phi[:, None]).reshape(E, C, 3)
-        G_Y += segment_sum((f[:, :, GROUP] * G_M[recv]).reshape(E, C * 9), send, N).reshape(N, C, 9)
-        GMr, Ys = G_M[recv], sv["Yc"][send]
-        g_f = np.stack([dot_I(GMr, Ys), dot_A(GMr, Ys), dot_S(GMr, Ys)], axis=-1)   # [E,C,3]
-        dft = radial_mlp_dd(P, l, rho, drho, sv["mlp_cache"]).reshape(E, C, 3)
-        ft3 = sv["ft"].reshape(E, C, 3)
-        g_d += (g_f * (dft * phi[:, None, None] + ft3 * dphi[:, None, None])).sum((1, 2))
+        G_Y = G_Y.reshape(N, C * 9)
+        for sl in chunks:
+            rho, drho = rho_of(sl)
+            ft, mlp_cache = radial_mlp(P, l, rho)
+            f = (ft * phi[sl, None]).reshape(-1, C, 3)
+            GMr, Ys = G_M[recv[sl]], sv["Yc"][send[sl]]
+            G_Y += segment_sum((f[:, :, GROUP] * GMr).reshape(-1, C * 9), send[sl], N)
+            g_f = np.stack([dot_I(GMr, Ys), dot_A(GMr, Ys), dot_S(GMr, Ys)], axis=-1)   # [e,C,3]
+            dft = radial_mlp_dd(P, l, rho, drho, mlp_cache).reshape(-1, C, 3)
+            ft3 = ft.reshape(-1, C, 3)
+            g_d[sl] += (g_f * (dft * phi[sl, None, None] + ft3 * dphi[sl, None, None])).sum((1, 2))
+        G_Y = G_Y.reshape(N, C, 9)
         G_Xh += mix3_T(T[:3], G_Y)
         nx, Xin = sv["nx"], sv["X"]
         GX = G_Xh / nx[:, :, None] - Xin * (2.0 * frob(G_Xh, Xin) / nx**2)[:, :, None]
@@ -471,20 +493,20 @@ def energy_forces_compact(params, cfg: OracleConfig, species, batch, pairs, delt
     g_n0 = _ln_bwd(g_e0 @ P["es0_w"], P["init_norm_g"], ln0_cache)                   # [N,C]
     G_X0 = mix3_T(P["et_w"], G_Xm) + 2.0 * g_n0[:, :, None] * X0
     # edge accumulation X0_i += w_e[:,grp] * basis_e
-    Gr = G_X0[recv]                                                                  # [E,C,9]
-    bI = np.zeros((E, 9)); bI[:, 0] = 1.0
-    bA = basis * gA
-    bS = basis * gS
-    g_w = np.stack([dot_I(Gr, bI[:, None, :]), dot_A(Gr, bA[:, None, :]),
-                    dot_S(Gr, bS[:, None, :])], axis=-1)                             # [E,C,3]
-    ddp = np.stack([drho @ P["dp_w"][k].T for k in range(3)], axis=-1)               # [E,C,3]
-    g_d += (g_w * Z[:, :, None] * (ddp * phi[:, None, None] + dpv * dphi[:, None, None])).sum((1, 2))
-    # d/du of  2*w2*(a_G . u)  and  w3 * u^T S_G u
-    wA = w[:, :, 1]
-    wS = w[:, :, 2]
-    g_u += 2.0 * np.einsum("ec,ecq->eq", wA, Gr[:, :, 1:4])
-    SG = to_full(Gr * gS)                                                            # [E,C,3,3]
-    g_u += 2.0 * np.einsum("ec,ecab,eb->ea", wS, SG, u)
+    for sl in chunks:
+        Z, dpv, ddp = embed_weights(sl)
+        w = dpv * (phi[sl, None] * Z)[:, :, None]
+        Gr = G_X0[recv[sl]]                                                          # [e,C,9]
+        bs = basis[sl]
+        bI = np.zeros_like(bs)
+        bI[:, 0] = 1.0
+        g_w = np.stack([dot_I(Gr, bI[:, None, :]), dot_A(Gr, (bs * gA)[:, None, :]),
+                        dot_S(Gr, (bs * gS)[:, None, :])], axis=-1)                  # [e,C,3]
+        g_d[sl] += (g_w * Z[:, :, None] * (ddp * phi[sl, None, None] + dpv * dphi[sl, None, None])).sum((1, 2))
+        # d/du of  2*w2*(a_G . u)  and  w3 * u^T S_G u
+        g_u[sl] += 2.0 * np.einsum("ec,ecq->eq", w[:, :, 1], Gr[:, :, 1:4])
+        SG = to_full(Gr * gS)                                                        # [e,C,3,3]
+        g_u[sl] += 2.0 * np.einsum("ec,ecab,eb->ea", w[:, :, 2], SG, u[sl])
     g_u[loop] = 0.0
 
     # pullback: d = |delta|, u = delta/d

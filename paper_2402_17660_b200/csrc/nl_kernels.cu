@@ -1,0 +1,665 @@
+// Cutoff neighbor search for sm_100a: cell binning, deterministic counting sort of atoms by
+// cell, and a warp-per-atom scan of the 27 surrounding cells (or of the atom's own sample for
+// the brute strategy) that emits a CSR structure sorted by (i, j).
+//
+// Replaces, with identical results, the reference's
+//   neighbors.py:103-133   grid construction + cell sort
+//   _neighbor_kernels.py:24-233   brute/cell x open/wrapped pair kernels
+//   neighbors.py:204-225   overflow count, full-list mirror, self loops, lexsort
+//
+// Exactness: every accept/reject decision and every emitted delta/distance is computed in
+// float64 with the reference's operation order (d = r_i - r_j for i < j, reduce c then b
+// then a with rint(component/diagonal), d2 = (dx*dx + dy*dy) + dz*dz, window on squared
+// distances) using __dmul_rn/__dadd_rn/__dsub_rn so that no FMA is contracted.  Mirrored rows
+// (j, i) are the exact negation, as in neighbors.py:209-212.
+//
+// Two passes over the candidates (count -> exclusive scan -> fill) give each row its final
+// offset without atomics, so the output order is deterministic and equals np.lexsort((j, i)).
+#include <algorithm>
+
+#include "nnp_common.cuh"
+
+namespace {
+
+constexpr int NL_THREADS = 256;
+constexpr int NL_WARPS = NL_THREADS / 32;
+constexpr int NL_MAXROW = 256;  // row entries kept in shared memory; longer rows use scratch
+
+struct GridDev {
+    int dims[3];
+    int ncell;
+    double low[3];
+    double inv_edge[3];
+};
+
+struct Metric {
+    int wrapped;
+    double b00, b10, b11, b20, b21, b22;
+    double i00, i11, i22;
+    double lo2, hi2;
+};
+
+struct NlArgs {
+    int n, n_samples, capacity, strategy, flags, periodic, max_cells;
+    double cutoff;
+    double inv_box[9];
+    int host_dims[3];
+    Metric metric;
+    const double *pos;
+    const int *batch;
+    // workspace
+    int *cell_id, *cell_start, *cell_cursor, *tmp_order, *sidx, *rank_of, *sbatch, *row_count;
+    int *sample_ptr, *scratch_col, *scratch_t;
+    double *spos;
+    double *bounds_partial;
+    GridDev *grid;
+    // outputs
+    int *pairs, *row_ptr, *order, *counts;
+    void *deltas, *dists;
+};
+
+__device__ __forceinline__ double rint_div(double x, double diag, double inv_diag)
+{
+    double q = x * inv_diag;
+    double r = rint(q);
+    // the reciprocal product can only disagree with the true quotient next to a tie
+    if (fabs(fabs(q - r) - 0.5) < 1e-6) r = rint(x / diag);
+    return r;
+}
+
+// Displacement r_lo - r_hi of the pair ordered by ORIGINAL index (as the reference computes
+// it), reduced to the minimum image; returns the squared norm.
+__device__ __forceinline__ double pair_delta(const Metric &m, double ax, double ay, double az,
+                                             double bx, double by, double bz, double &dx,
+                                             double &dy, double &dz)
+{
+    dx = __dsub_rn(ax, bx);
+    dy = __dsub_rn(ay, by);
+    dz = __dsub_rn(az, bz);
+    if (m.wrapped) {
+        double s = rint_div(dz, m.b22, m.i22);
+        dx = __dsub_rn(dx, __dmul_rn(s, m.b20));
+        dy = __dsub_rn(dy, __dmul_rn(s, m.b21));
+        dz = __dsub_rn(dz, __dmul_rn(s, m.b22));
+        s = rint_div(dy, m.b11, m.i11);
+        dx = __dsub_rn(dx, __dmul_rn(s, m.b10));
+        dy = __dsub_rn(dy, __dmul_rn(s, m.b11));
+        dx = __dsub_rn(dx, __dmul_rn(m.b00, rint_div(dx, m.b00, m.i00)));
+    }
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+__global__ void k_fill_i32(int *p, int64_t n, int v)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_sample_ptr(const int *__restrict__ batch, int n, int n_samples,
+                             int *__restrict__ sample_ptr)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int b = batch[i];
+    if (i == 0 || batch[i - 1] != b) sample_ptr[b] = i;
+    if (i == n - 1) sample_ptr[n_samples] = n;
+}
+
+// ---- open-boundary grid: bounding box reduction (neighbors.py:116-124)
+__global__ void k_bounds_partial(const double *__restrict__ pos, int n, double *__restrict__ partial)
+{
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double v = pos[3 * (size_t)i + k];
+            lo[k] = fmin(lo[k], v);
+            hi[k] = fmax(hi[k], v);
+        }
+    }
+    __shared__ double s[NL_WARPS][6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[k] = fmin(lo[k], __shfl_xor_sync(NNP_FULL_MASK, lo[k], o));
+            hi[k] = fmax(hi[k], __shfl_xor_sync(NNP_FULL_MASK, hi[k], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k < 3; ++k) {
+            s[threadIdx.x >> 5][k] = lo[k];
+            s[threadIdx.x >> 5][3 + k] = hi[k];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double v = s[0][threadIdx.x];
+        for (int w = 1; w < NL_WARPS; ++w)
+            v = threadIdx.x < 3 ? fmin(v, s[w][threadIdx.x]) : fmax(v, s[w][threadIdx.x]);
+        partial[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+__global__ void k_grid_setup(NlArgs a, int n_partial)
+{
+    if (threadIdx.x != 0) return;
+    GridDev g;
+    if (a.periodic) {
+        for (int k = 0; k < 3; ++k) {
+            g.dims[k] = a.host_dims[k];
+            g.low[k] = 0.0;
+            g.inv_edge[k] = 0.0;
+        }
+    } else {
+        double lo[3], hi[3];
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = a.bounds_partial[k];
+            hi[k] = a.bounds_partial[3 + k];
+        }
+        for (int b = 1; b < n_partial; ++b)
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = fmin(lo[k], a.bounds_partial[b * 6 + k]);
+                hi[k] = fmax(hi[k], a.bounds_partial[b * 6 + 3 + k]);
+            }
+        double extent[3];
+        for (int k = 0; k < 3; ++k) {
+            g.low[k] = lo[k] - 0.5 * a.cutoff;
+            extent[k] = hi[k] - g.low[k] + 0.5 * a.cutoff;
+            double d = floor(extent[k] / a.cutoff);
+            g.dims[k] = d < 1.0 ? 1 : (d > 1.0e6 ? 1000000 : (int)d);
+        }
+        // never more cells than the workspace holds: coarsen the longest axis (cells only grow,
+        // so the 27-cell neighbourhood still covers the cutoff)
+        while ((int64_t)g.dims[0] * g.dims[1] * g.dims[2] > (int64_t)a.max_cells) {
+            int k = 0;
+            if (g.dims[1] > g.dims[k]) k = 1;
+            if (g.dims[2] > g.dims[k]) k = 2;
+            g.dims[k] = (g.dims[k] + 1) / 2;
+        }
+        for (int k = 0; k < 3; ++k) g.inv_edge[k] = (double)g.dims[k] / extent[k];
+    }
+    g.ncell = g.dims[0] * g.dims[1] * g.dims[2];
+    *a.grid = g;
+    a.counts[2] = g.ncell;
+}
+
+__global__ void k_cell_assign(NlArgs a)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const GridDev g = *a.grid;
+    double x = a.pos[3 * (size_t)i], y = a.pos[3 * (size_t)i + 1], z = a.pos[3 * (size_t)i + 2];
+    int c[3];
+    if (a.periodic) {
+        // fractional coordinates, wrapped into [0,1)  (neighbors.py:110-112)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double f = x * a.inv_box[k] + y * a.inv_box[3 + k] + z * a.inv_box[6 + k];
+            f -= floor(f);
+            int v = (int)floor(f * g.dims[k]);
+            c[k] = v < 0 ? 0 : (v >= g.dims[k] ? g.dims[k] - 1 : v);
+        }
+    } else {
+        double p[3] = {x, y, z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            int v = (int)floor((p[k] - g.low[k]) * g.inv_edge[k]);
+            c[k] = v < 0 ? 0 : (v >= g.dims[k] ? g.dims[k] - 1 : v);
+        }
+    }
+    int flat = (c[0] * g.dims[1] + c[1]) * g.dims[2] + c[2];
+    a.cell_id[i] = flat;
+    atomicAdd(&a.cell_start[flat], 1);  // counts; turned into starts by the scan that follows
+}
+
+__global__ void k_cell_scatter(NlArgs a)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    int c = a.cell_id[i];
+    int slot = a.cell_start[c] + atomicAdd(&a.cell_cursor[c], 1);
+    a.tmp_order[slot] = i;
+}
+
+// Stable order inside each cell (ascending original index), so the sort equals
+// np.argsort(flat, kind="stable") (neighbors.py:129) whatever order the atomics ran in.
+__global__ void k_cell_rank(NlArgs a)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    int c = a.cell_id[i];
+    int p0 = a.cell_start[c], p1 = a.cell_start[c + 1];
+    int rank = 0;
+    for (int t = p0; t < p1; ++t) rank += (a.tmp_order[t] < i);
+    int s = p0 + rank;
+    a.sidx[s] = i;
+    a.rank_of[i] = s;
+    a.sbatch[s] = a.batch[i];
+    a.spos[3 * (size_t)s] = a.pos[3 * (size_t)i];
+    a.spos[3 * (size_t)s + 1] = a.pos[3 * (size_t)i + 1];
+    a.spos[3 * (size_t)s + 2] = a.pos[3 * (size_t)i + 2];
+}
+
+__global__ void k_identity_order(NlArgs a)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    a.sidx[i] = i;
+    a.rank_of[i] = i;
+    a.sbatch[i] = a.batch[i];
+    a.spos[3 * (size_t)i] = a.pos[3 * (size_t)i];
+    a.spos[3 * (size_t)i + 1] = a.pos[3 * (size_t)i + 1];
+    a.spos[3 * (size_t)i + 2] = a.pos[3 * (size_t)i + 2];
+}
+
+// Candidate runs [p0, p1) in sorted-atom space for the atom at sorted position s.
+template <typename F>
+__device__ __forceinline__ void visit_runs(const NlArgs &a, const GridDev &g, int cell, int bi, F &&f)
+{
+    if (a.strategy == NNP_STRATEGY_BRUTE) {
+        // same-sample atoms are contiguous (system.py:231-235); foreign samples can never pair
+        f(a.sample_ptr[bi], a.sample_ptr[bi + 1]);
+        return;
+    }
+    const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
+    const int c2 = cell % m2;
+    const int c1 = (cell / m2) % m1;
+    const int c0 = cell / (m1 * m2);
+    for (int o0 = -1; o0 <= 1; ++o0) {
+        int n0 = c0 + o0;
+        if (a.periodic) {
+            n0 = n0 < 0 ? n0 + m0 : (n0 >= m0 ? n0 - m0 : n0);
+        } else if (n0 < 0 || n0 >= m0) {
+            continue;
+        }
+        for (int o1 = -1; o1 <= 1; ++o1) {
+            int n1 = c1 + o1;
+            if (a.periodic) {
+                n1 = n1 < 0 ? n1 + m1 : (n1 >= m1 ? n1 - m1 : n1);
+            } else if (n1 < 0 || n1 >= m1) {
+                continue;
+            }
+            const int base = (n0 * m1 + n1) * m2;
+            int lo = c2 - 1, hi = c2 + 1;
+            if (a.periodic) {
+                // three cells along the fastest axis are contiguous in the sorted order except
+                // where they wrap (the periodic grid has >= 3 cells per axis)
+                if (lo < 0) {
+                    f(a.cell_start[base + m2 - 1], a.cell_start[base + m2]);
+                    lo = 0;
+                }
+                if (hi >= m2) {
+                    f(a.cell_start[base], a.cell_start[base + 1]);
+                    hi = m2 - 1;
+                }
+            } else {
+                lo = lo < 0 ? 0 : lo;
+                hi = hi >= m2 ? m2 - 1 : hi;
+            }
+            f(a.cell_start[base + lo], a.cell_start[base + hi + 1]);
+        }
+    }
+}
+
+template <bool FILL, typename OutT>
+__global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
+{
+    __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
+    __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int s = blockIdx.x * NL_WARPS + wib;
+    if (s >= a.n) return;
+    if (FILL && a.row_ptr[a.n] > a.capacity) return;  // overflow: host raises CapacityError
+
+    const bool full = a.flags & NNP_NL_FULL_LIST;
+    const bool renumber = a.flags & NNP_NL_RENUMBER;
+    const int io = a.sidx[s];
+    const int bi = a.sbatch[s];
+    const int row = renumber ? s : io;
+    const double ax = a.spos[3 * (size_t)s], ay = a.spos[3 * (size_t)s + 1],
+                 az = a.spos[3 * (size_t)s + 2];
+    const Metric m = a.metric;
+
+    int *list_col = nullptr, *list_t = nullptr;
+    int row_start = 0;
+    if (FILL) {
+        row_start = a.row_ptr[row];
+        const int expect = a.row_ptr[row + 1] - row_start;
+        if (expect <= NL_MAXROW) {
+            list_col = s_col[wib];
+            list_t = s_t[wib];
+        } else {
+            list_col = a.scratch_col + row_start;
+            list_t = a.scratch_t + row_start;
+        }
+    }
+
+    int cnt = 0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    auto process = [&](int p0, int p1) {
+        for (int base = p0; base < p1; base += 32) {
+            const int t = base + lane;
+            bool ok = false;
+            int jo = 0;
+            if (t < p1) {
+                jo = a.sidx[t];
+                if (a.sbatch[t] == bi && jo != io && (full || jo > io)) {
+                    const double bx = a.spos[3 * (size_t)t], by = a.spos[3 * (size_t)t + 1],
+                                 bz = a.spos[3 * (size_t)t + 2];
+                    double dx, dy, dz, d2;
+                    if (io < jo)
+                        d2 = pair_delta(m, ax, ay, az, bx, by, bz, dx, dy, dz);
+                    else
+                        d2 = pair_delta(m, bx, by, bz, ax, ay, az, dx, dy, dz);
+                    ok = d2 > m.lo2 && d2 <= m.hi2;
+                }
+            }
+            const unsigned hit = __ballot_sync(NNP_FULL_MASK, ok);
+            if (FILL && ok) {
+                const int p = cnt + __popc(hit & lt_mask);
+                list_col[p] = renumber ? t : jo;
+                list_t[p] = t;
+            }
+            cnt += __popc(hit);
+        }
+    };
+    GridDev g{};
+    int cell = 0;
+    if (a.strategy == NNP_STRATEGY_CELL) {
+        g = *a.grid;
+        cell = a.cell_id[io];
+    }
+    visit_runs(a, g, cell, bi, process);
+
+    if (a.flags & NNP_NL_SELF_LOOPS) {
+        if (FILL && lane == 0) {
+            list_col[cnt] = row;
+            list_t[cnt] = s;
+        }
+        cnt += 1;
+    }
+
+    if (!FILL) {
+        if (lane == 0) {
+            a.row_count[row] = cnt;
+            atomicMax(&a.counts[1], cnt);
+        }
+        return;
+    }
+
+    __syncwarp();
+    OutT *deltas = static_cast<OutT *>(a.deltas);
+    OutT *dists = static_cast<OutT *>(a.dists);
+    for (int e = lane; e < cnt; e += 32) {
+        const int col = ((volatile int *)list_col)[e];
+        const int t = ((volatile int *)list_t)[e];
+        int rank = 0;
+        for (int q = 0; q < cnt; ++q) rank += (((volatile int *)list_col)[q] < col);
+        const size_t idx = (size_t)row_start + rank;
+        a.pairs[2 * idx] = row;
+        a.pairs[2 * idx + 1] = col;
+        double dx = 0.0, dy = 0.0, dz = 0.0, dist = 0.0;
+        if (t != s) {
+            const int jo = a.sidx[t];
+            const double bx = a.spos[3 * (size_t)t], by = a.spos[3 * (size_t)t + 1],
+                         bz = a.spos[3 * (size_t)t + 2];
+            double d2;
+            if (io < jo) {
+                d2 = pair_delta(m, ax, ay, az, bx, by, bz, dx, dy, dz);
+            } else {
+                d2 = pair_delta(m, bx, by, bz, ax, ay, az, dx, dy, dz);
+                dx = -dx;
+                dy = -dy;
+                dz = -dz;
+            }
+            dist = sqrt(d2);
+        }
+        deltas[3 * idx] = (OutT)dx;
+        deltas[3 * idx + 1] = (OutT)dy;
+        deltas[3 * idx + 2] = (OutT)dz;
+        dists[idx] = (OutT)dist;
+    }
+}
+
+__global__ void k_total(NlArgs a)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) a.counts[0] = a.row_ptr[a.n];
+}
+
+template <typename OutT>
+__global__ void k_pad_tail(NlArgs a)
+{
+    const int total = a.row_ptr[a.n];
+    const int64_t idx = (int64_t)total + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (total > a.capacity || idx >= a.capacity) return;
+    a.pairs[2 * idx] = -1;
+    a.pairs[2 * idx + 1] = -1;
+    OutT *deltas = static_cast<OutT *>(a.deltas);
+    OutT *dists = static_cast<OutT *>(a.dists);
+    deltas[3 * idx] = deltas[3 * idx + 1] = deltas[3 * idx + 2] = (OutT)0;
+    dists[idx] = (OutT)0;
+}
+
+__global__ void k_copy_order(NlArgs a)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.n) a.order[i] = (a.flags & NNP_NL_RENUMBER) ? a.sidx[i] : i;
+}
+
+__global__ void k_f32_to_f64(const float *__restrict__ src, double *__restrict__ dst, int64_t n)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (double)src[i];
+}
+
+__global__ void k_pullback(const int *__restrict__ pairs, const double *__restrict__ deltas,
+                           const double *__restrict__ dists, const double *__restrict__ g, int count,
+                           double *__restrict__ grad, int *__restrict__ flag)
+{
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    int i = pairs[2 * e], j = pairs[2 * e + 1];
+    if (i == j || i < 0) return;
+    double d = dists[e];
+    if (d == 0.0) {
+        atomicMin(flag, e + 1);  // first offending row, like the reference's report
+        return;
+    }
+    double ge = g[e];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double c = ge * (deltas[3 * (size_t)e + k] / d);
+        atomicAdd(&grad[3 * (size_t)i + k], c);
+        atomicAdd(&grad[3 * (size_t)j + k], -c);
+    }
+}
+
+constexpr int BOUNDS_BLOCKS = 128;
+
+size_t carve(NlArgs &a, const nnp_nl_params *p, void *ws)
+{
+    NnpArena ar(ws);
+    const size_t n = (size_t)p->n_atoms;
+    const size_t mc = (size_t)(p->max_cells > 0 ? p->max_cells : 1);
+    a.cell_id = ar.take<int>(n);
+    a.cell_start = ar.take<int>(mc + 1);
+    a.cell_cursor = ar.take<int>(mc);
+    a.tmp_order = ar.take<int>(n);
+    a.sidx = ar.take<int>(n);
+    a.rank_of = ar.take<int>(n);
+    a.sbatch = ar.take<int>(n);
+    a.row_count = ar.take<int>(n + 1 + nnp_scan_temp_ints((int64_t)std::max(n, mc) + 1));
+    a.sample_ptr = ar.take<int>((size_t)p->n_samples + 1);
+    a.scratch_col = ar.take<int>((size_t)p->capacity);
+    a.scratch_t = ar.take<int>((size_t)p->capacity);
+    a.spos = ar.take<double>(3 * n);
+    a.bounds_partial = ar.take<double>(6 * BOUNDS_BLOCKS);
+    a.grid = ar.take<GridDev>(1);
+    return ar.bytes();
+}
+
+int validate(const nnp_nl_params *p)
+{
+    NNP_CHECK_ARG(p != nullptr, "params is NULL");
+    NNP_CHECK_ARG(p->n_atoms >= 1, "n_atoms must be >= 1");
+    NNP_CHECK_ARG(p->n_samples >= 1, "n_samples must be >= 1");
+    NNP_CHECK_ARG(p->capacity >= 1, "capacity must be >= 1");
+    NNP_CHECK_ARG(p->cutoff_lower >= 0.0 && p->cutoff_lower < p->cutoff_upper,
+                  "cutoffs must satisfy 0 <= cutoff_lower < cutoff_upper");
+    NNP_CHECK_ARG(p->box_kind >= 0 && p->box_kind <= 2, "unknown box kind");
+    NNP_CHECK_ARG(p->strategy == NNP_STRATEGY_BRUTE || p->strategy == NNP_STRATEGY_CELL,
+                  "strategy must be brute or cell");
+    if (p->strategy == NNP_STRATEGY_CELL) {
+        NNP_CHECK_ARG(p->max_cells >= 1, "max_cells must be >= 1 for the cell strategy");
+        if (p->box_kind != NNP_BOX_NONE) {
+            NNP_CHECK_ARG(p->grid_dims[0] >= 3 && p->grid_dims[1] >= 3 && p->grid_dims[2] >= 3,
+                          "periodic cell grid needs >= 3 cells per axis");
+            NNP_CHECK_ARG((int64_t)p->grid_dims[0] * p->grid_dims[1] * p->grid_dims[2] <=
+                              (int64_t)p->max_cells,
+                          "grid_dims exceed max_cells");
+        }
+    }
+    if (p->box_kind != NNP_BOX_NONE)
+        NNP_CHECK_ARG(p->box[0] > 0 && p->box[4] > 0 && p->box[8] > 0,
+                      "box diagonal must be positive");
+    return NNP_OK;
+}
+
+}  // namespace
+
+extern "C" int nnp_nl_workspace_bytes(const nnp_nl_params *p, size_t *bytes)
+{
+    int rc = validate(p);
+    if (rc) return rc;
+    NNP_CHECK_ARG(bytes != nullptr, "bytes is NULL");
+    NlArgs a{};
+    *bytes = carve(a, p, nullptr);
+    return NNP_OK;
+}
+
+extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int32_t *batch,
+                            int32_t *pairs, void *deltas, void *dists, int32_t *row_ptr,
+                            int32_t *order, int32_t *counts, void *workspace,
+                            size_t workspace_bytes, nnp_stream_t stream_)
+{
+    int rc = validate(p);
+    if (rc) return rc;
+    NNP_CHECK_ARG(pos && batch && pairs && deltas && dists && counts && workspace,
+                  "NULL buffer passed to nnp_nl_build");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    NlArgs a{};
+    size_t need = carve(a, p, workspace);
+    if (need > workspace_bytes) {
+        nnp_set_error("workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+        return NNP_ERR_WORKSPACE;
+    }
+    a.n = p->n_atoms;
+    a.n_samples = p->n_samples;
+    a.capacity = p->capacity;
+    a.strategy = p->strategy;
+    a.flags = p->flags;
+    a.periodic = p->box_kind != NNP_BOX_NONE;
+    a.max_cells = p->max_cells > 0 ? p->max_cells : 1;
+    a.cutoff = p->cutoff_upper;
+    for (int k = 0; k < 9; ++k) a.inv_box[k] = p->inv_box[k];
+    for (int k = 0; k < 3; ++k) a.host_dims[k] = p->grid_dims[k];
+    Metric &m = a.metric;
+    m.wrapped = a.periodic;
+    m.lo2 = p->cutoff_lower * p->cutoff_lower;
+    m.hi2 = p->cutoff_upper * p->cutoff_upper;
+    if (a.periodic) {
+        m.b00 = p->box[0];
+        m.b10 = p->box[3];
+        m.b11 = p->box[4];
+        m.b20 = p->box[6];
+        m.b21 = p->box[7];
+        m.b22 = p->box[8];
+        m.i00 = 1.0 / m.b00;
+        m.i11 = 1.0 / m.b11;
+        m.i22 = 1.0 / m.b22;
+    }
+    a.pos = pos;
+    a.batch = batch;
+    a.pairs = pairs;
+    a.deltas = deltas;
+    a.dists = dists;
+    a.row_ptr = row_ptr ? row_ptr : a.row_count;
+    a.order = order;
+    a.counts = counts;
+    int *scan_temp = a.row_count + a.n + 1;
+
+    const int n = a.n;
+    const int nb = nnp_blocks(n, 256);
+    cudaMemsetAsync(counts, 0, 4 * sizeof(int), stream);
+    k_fill_i32<<<nnp_blocks(a.n_samples + 1, 256), 256, 0, stream>>>(a.sample_ptr, a.n_samples + 1, n);
+    k_sample_ptr<<<nb, 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr);
+
+    if (a.strategy == NNP_STRATEGY_CELL) {
+        int n_partial = 1;
+        if (!a.periodic) {
+            n_partial = std::min(BOUNDS_BLOCKS, nb);
+            k_bounds_partial<<<n_partial, NL_THREADS, 0, stream>>>(pos, n, a.bounds_partial);
+        }
+        k_grid_setup<<<1, 32, 0, stream>>>(a, n_partial);
+        cudaMemsetAsync(a.cell_start, 0, ((size_t)a.max_cells + 1) * sizeof(int), stream);
+        cudaMemsetAsync(a.cell_cursor, 0, (size_t)a.max_cells * sizeof(int), stream);
+        k_cell_assign<<<nb, 256, 0, stream>>>(a);
+        rc = nnp_exclusive_scan_i32(a.cell_start, a.cell_start, (int64_t)a.max_cells + 1, scan_temp,
+                                    stream);
+        if (rc) return rc;
+        k_cell_scatter<<<nb, 256, 0, stream>>>(a);
+        k_cell_rank<<<nb, 256, 0, stream>>>(a);
+    } else {
+        k_identity_order<<<nb, 256, 0, stream>>>(a);
+    }
+    NNP_CHECK_LAUNCH("neighbor binning");
+
+    const int row_blocks = nnp_blocks(n, NL_WARPS);
+    const bool f32 = p->flags & NNP_NL_F32_OUT;
+    k_rows<false, double><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+    // row_count has n entries; entry n must be zero so the scan's last output is the total
+    cudaMemsetAsync(a.row_count + n, 0, sizeof(int), stream);
+    rc = nnp_exclusive_scan_i32(a.row_count, a.row_ptr, (int64_t)n + 1, scan_temp, stream);
+    if (rc) return rc;
+    k_total<<<1, 32, 0, stream>>>(a);
+    if (f32)
+        k_rows<true, float><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+    else
+        k_rows<true, double><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+    if (!(p->flags & NNP_NL_NO_PAD)) {
+        if (f32)
+            k_pad_tail<float><<<nnp_blocks(a.capacity, 256), 256, 0, stream>>>(a);
+        else
+            k_pad_tail<double><<<nnp_blocks(a.capacity, 256), 256, 0, stream>>>(a);
+    }
+    if (order) k_copy_order<<<nb, 256, 0, stream>>>(a);
+    NNP_CHECK_LAUNCH("neighbor rows");
+    return NNP_OK;
+}
+
+extern "C" int nnp_f32_to_f64(const float *src, double *dst, int64_t n, nnp_stream_t stream)
+{
+    NNP_CHECK_ARG(src && dst && n >= 0, "bad arguments to nnp_f32_to_f64");
+    if (n == 0) return NNP_OK;
+    k_f32_to_f64<<<nnp_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+    NNP_CHECK_LAUNCH("f32_to_f64");
+    return NNP_OK;
+}
+
+extern "C" int nnp_distance_pullback(const int32_t *pairs, const double *deltas,
+                                     const double *dists, const double *g, int32_t count,
+                                     int32_t n_atoms, double *grad, int32_t *flag_out,
+                                     nnp_stream_t stream_)
+{
+    NNP_CHECK_ARG(pairs && deltas && dists && g && grad && flag_out && count >= 0 && n_atoms >= 1,
+                  "bad arguments to nnp_distance_pullback");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    cudaMemsetAsync(grad, 0, 3 * (size_t)n_atoms * sizeof(double), stream);
+    cudaMemsetAsync(flag_out, 0x7f, sizeof(int), stream);  // 0x7f7f7f7f = none
+    if (count > 0)
+        k_pullback<<<nnp_blocks(count, 256), 256, 0, stream>>>(pairs, deltas, dists, g, count, grad,
+                                                              flag_out);
+    NNP_CHECK_LAUNCH("distance_pullback");
+    return NNP_OK;
+}

@@ -1,0 +1,120 @@
+// Exclusive prefix sum of int32 arrays: block-local scan, scan of block totals, add-back.
+// Used for cell starts (neighbors.py:127-133 does bincount + cumsum) and CSR row offsets.
+#include <stdarg.h>
+
+#include "nnp_common.cuh"
+
+static thread_local char g_last_error[512] = "";
+
+void nnp_set_error(const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+}
+
+extern "C" const char *nnp_last_error(void) { return g_last_error; }
+extern "C" int nnp_version(void) { return 100; }
+
+namespace {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *total)
+{
+    __shared__ int warp_sums[SCAN_THREADS / 32];
+    __shared__ int block_total;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(NNP_FULL_MASK, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < SCAN_THREADS / 32 ? warp_sums[lane] : 0;
+        int winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(NNP_FULL_MASK, winc, o);
+            if (lane >= o) winc += t;
+        }
+        if (lane < SCAN_THREADS / 32) warp_sums[lane] = winc - w;
+        if (lane == 31) block_total = winc;
+    }
+    __syncthreads();
+    *total = block_total;
+    int result = warp_sums[wid] + inc - v;
+    __syncthreads();
+    return result;
+}
+
+__global__ void scan_tiles(const int32_t *in, int32_t *out, int64_t n, int32_t *tile_totals)
+{
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int v[SCAN_ITEMS];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        sum += v[k];
+    }
+    int total;
+    int prefix = block_exclusive_scan(sum, &total);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        if (base + k < n) out[base + k] = prefix;
+        prefix += v[k];
+    }
+    if (threadIdx.x == 0) tile_totals[blockIdx.x] = total;
+}
+
+__global__ void scan_totals(int32_t *tile_totals, int nt)
+{
+    __shared__ int carry_s;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < nt; base += SCAN_THREADS) {
+        int idx = base + threadIdx.x;
+        int v = idx < nt ? tile_totals[idx] : 0;
+        int total;
+        int prefix = block_exclusive_scan(v, &total);
+        int carry = carry_s;
+        if (idx < nt) tile_totals[idx] = carry + prefix;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + total;
+        __syncthreads();
+    }
+}
+
+__global__ void scan_add(int32_t *__restrict__ out, int64_t n, const int32_t *__restrict__ tile_totals)
+{
+    const int add = tile_totals[blockIdx.x];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k)
+        if (base + k < n) out[base + k] += add;
+}
+
+}  // namespace
+
+size_t nnp_scan_temp_ints(int64_t n) { return (size_t)((n + SCAN_TILE - 1) / SCAN_TILE) + 1; }
+
+int nnp_exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, int32_t *temp,
+                           cudaStream_t stream)
+{
+    if (n <= 0) return NNP_OK;
+    const int nt = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
+    scan_tiles<<<nt, SCAN_THREADS, 0, stream>>>(in, out, n, temp);
+    if (nt > 1) {
+        scan_totals<<<1, SCAN_THREADS, 0, stream>>>(temp, nt);
+        scan_add<<<nt, SCAN_THREADS, 0, stream>>>(out, n, temp);
+    }
+    NNP_CHECK_LAUNCH("exclusive_scan");
+    return NNP_OK;
+}

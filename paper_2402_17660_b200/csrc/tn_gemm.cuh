@@ -1,0 +1,228 @@
+// Node-level channel-mixing GEMMs:  out[r, n] = sum_k A[r, k] * W[n, k]   ("NT": both K-contiguous).
+//
+// These are the only dense contractions of the TensorNet step (the per-node linears of SURVEY.md
+// Appendix A: lt0..lt5, the embedding's scalar MLP, the readout).  Rows can be addressed through
+// the [node][9][C] tensor layout so that all I rows, all A rows or all S rows of a node tensor form
+// one GEMM with one weight matrix.
+//
+// Two inner loops behind one interface:
+//   MMA = true : tensor cores with the 3xTF32 split (a = a_hi + a_lo, both TF32; the product keeps
+//                a_lo*b_hi + a_hi*b_lo + a_hi*b_hi in an FP32 accumulator) -> FP32-level accuracy.
+//   MMA = false: plain FP32 FFMA, kept as the numerical cross-check of the split.
+#pragma once
+
+#include "nnp_common.cuh"
+#include "tn_math.cuh"
+
+enum { PRO_NONE = 0, PRO_SILU = 1 };
+enum { EPI_STORE = 0, EPI_MUL_SILU_GRAD = 1, EPI_GATE = 2, EPI_ADD = 3 };
+
+struct GemmArgs {
+    const float *A;
+    const float *W;
+    const float *bias;
+    float *out;
+    float *out2;
+    const float *aux;
+    int M, N, K;
+    int lda, ldo, ldaux;
+    int ncomp, q0, grp;  // ncomp > 0: logical row r -> physical row (r / ncomp) * 9 + q0 + r % ncomp
+};
+
+struct GemmBatch {
+    GemmArgs g[3];
+};
+
+constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 32, GEMM_LD = GEMM_BK + 4, GEMM_THREADS = 256;
+
+__device__ __forceinline__ int gemm_phys_row(const GemmArgs &g, int r)
+{
+    if (g.ncomp == 0) return r;
+    const int node = r / g.ncomp;
+    return node * 9 + g.q0 + (r - node * g.ncomp);
+}
+
+__device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
+{
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float rest = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(rest));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2])
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <int EPI>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs &g, int r, int c, float v)
+{
+    if (r >= g.M || c >= g.N) return;
+    const int pr = gemm_phys_row(g, r);
+    if (g.bias) v += g.bias[c];
+    const size_t o = (size_t)pr * g.ldo + c;
+    if (EPI == EPI_STORE) {
+        g.out[o] = v;
+    } else if (EPI == EPI_MUL_SILU_GRAD) {
+        g.out[o] = v * nnp_silu_grad(g.aux[(size_t)pr * g.ldaux + c]);
+    } else if (EPI == EPI_GATE) {
+        const int node = g.ncomp ? r / g.ncomp : r;
+        g.out2[o] = v;
+        g.out[o] = v * nnp_silu(g.aux[(size_t)node * g.ldaux + 3 * c + g.grp]);
+    } else {
+        g.out[o] = v + g.aux[(size_t)pr * g.ldaux + c];
+    }
+}
+
+template <int PRO, int EPI, bool MMA>
+__global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
+{
+    const GemmArgs g = batch.g[blockIdx.z];
+    const int m0 = blockIdx.x * GEMM_BM;
+    const int n0 = blockIdx.y * GEMM_BN;
+    if (m0 >= g.M || n0 >= g.N) return;
+
+    __shared__ __align__(16) float As[GEMM_BM][GEMM_LD];
+    __shared__ __align__(16) float Ws[GEMM_BN][GEMM_LD];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    // tile loaders: 2 float4 per thread for each operand
+    int a_row[2], a_k4[2];
+    const float *a_ptr[2];
+    const float *w_ptr[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int idx = tid + i * GEMM_THREADS;
+        a_row[i] = idx >> 3;
+        a_k4[i] = (idx & 7) * 4;
+        const int r = m0 + a_row[i];
+        a_ptr[i] = r < g.M ? g.A + (size_t)gemm_phys_row(g, r) * g.lda + a_k4[i] : nullptr;
+        const int n = n0 + a_row[i];
+        w_ptr[i] = n < g.N ? g.W + (size_t)n * g.K + a_k4[i] : nullptr;
+    }
+
+    // MMA mapping: 8 warps as 2 (rows) x 4 (cols); warp tile 32 x 16 = 2 x 2 m16n8 tiles
+    const int wm = warp >> 2, wn = warp & 3;
+    const int gid = lane >> 2, tig = lane & 3;
+    // FFMA mapping: thread tile 4 rows x 4 (strided) cols
+    const int ty = tid >> 4, tx = tid & 15;
+
+    float acc[2][2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0f;
+
+    for (int k0 = 0; k0 < g.K; k0 += GEMM_BK) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float4 av = make_float4(0.f, 0.f, 0.f, 0.f), wv = av;
+            const bool k_ok = k0 + a_k4[i] < g.K;
+            if (a_ptr[i] && k_ok) av = *reinterpret_cast<const float4 *>(a_ptr[i] + k0);
+            if (w_ptr[i] && k_ok) wv = *reinterpret_cast<const float4 *>(w_ptr[i] + k0);
+            if (PRO == PRO_SILU) {
+                av.x = nnp_silu(av.x);
+                av.y = nnp_silu(av.y);
+                av.z = nnp_silu(av.z);
+                av.w = nnp_silu(av.w);
+            }
+            *reinterpret_cast<float4 *>(&As[a_row[i]][a_k4[i]]) = av;
+            *reinterpret_cast<float4 *>(&Ws[a_row[i]][a_k4[i]]) = wv;
+        }
+        __syncthreads();
+        if (MMA) {
+#pragma unroll
+            for (int kk = 0; kk < GEMM_BK; kk += 8) {
+                uint32_t ah[2][4], al[2][4], bh[2][2], bl[2][2];
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi) {
+                    const int rb = wm * 32 + mi * 16;
+                    tf32_split(As[rb + gid][kk + tig], ah[mi][0], al[mi][0]);
+                    tf32_split(As[rb + gid + 8][kk + tig], ah[mi][1], al[mi][1]);
+                    tf32_split(As[rb + gid][kk + tig + 4], ah[mi][2], al[mi][2]);
+                    tf32_split(As[rb + gid + 8][kk + tig + 4], ah[mi][3], al[mi][3]);
+                }
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) {
+                    const int cb = wn * 16 + ni * 8;
+                    tf32_split(Ws[cb + gid][kk + tig], bh[ni][0], bl[ni][0]);
+                    tf32_split(Ws[cb + gid][kk + tig + 4], bh[ni][1], bl[ni][1]);
+                }
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 2; ++ni) {
+                        mma_tf32(acc[mi][ni], al[mi], bh[ni]);
+                        mma_tf32(acc[mi][ni], ah[mi], bl[ni]);
+                        mma_tf32(acc[mi][ni], ah[mi], bh[ni]);
+                    }
+            }
+        } else {
+            // acc[i>>1][i&1][j] holds row ty*4+i, col tx+16*j
+#pragma unroll 8
+            for (int kk = 0; kk < GEMM_BK; ++kk) {
+                float a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = As[ty * 4 + i][kk];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = Ws[tx + 16 * j][kk];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i >> 1][i & 1][j] += a[i] * b[j];
+            }
+        }
+        __syncthreads();
+    }
+
+    if (MMA) {
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) {
+                const int r = m0 + wm * 32 + mi * 16 + gid;
+                const int c = n0 + wn * 16 + ni * 8 + tig * 2;
+                gemm_epilogue<EPI>(g, r, c, acc[mi][ni][0]);
+                gemm_epilogue<EPI>(g, r, c + 1, acc[mi][ni][1]);
+                gemm_epilogue<EPI>(g, r + 8, c, acc[mi][ni][2]);
+                gemm_epilogue<EPI>(g, r + 8, c + 1, acc[mi][ni][3]);
+            }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                gemm_epilogue<EPI>(g, m0 + ty * 4 + i, n0 + tx + 16 * j, acc[i >> 1][i & 1][j]);
+    }
+}
+
+extern int g_nnp_gemm_use_mma;  // 1 = 3xTF32 tensor cores (default), 0 = FP32 FFMA
+
+template <int PRO, int EPI>
+static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    int maxM = 0, maxN = 0;
+    for (int i = 0; i < count; ++i) {
+        maxM = b.g[i].M > maxM ? b.g[i].M : maxM;
+        maxN = b.g[i].N > maxN ? b.g[i].N : maxN;
+        if (b.g[i].K % 4 != 0 || b.g[i].lda % 4 != 0) {
+            nnp_set_error("gemm: K=%d and lda=%d must be multiples of 4", b.g[i].K, b.g[i].lda);
+            return NNP_ERR_INVALID;
+        }
+    }
+    if (maxM <= 0) return NNP_OK;
+    dim3 grid((maxM + GEMM_BM - 1) / GEMM_BM, (maxN + GEMM_BN - 1) / GEMM_BN, count);
+    if (g_nnp_gemm_use_mma)
+        gemm_nt_kernel<PRO, EPI, true><<<grid, GEMM_THREADS, 0, stream>>>(b);
+    else
+        gemm_nt_kernel<PRO, EPI, false><<<grid, GEMM_THREADS, 0, stream>>>(b);
+    NNP_CHECK_LAUNCH("gemm_nt");
+    return NNP_OK;
+}

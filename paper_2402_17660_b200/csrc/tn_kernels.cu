@@ -1,0 +1,1055 @@
+// TensorNet energy-and-forces step on sm_100a (oracle/tensornet_oracle.py
+// `energy_forces_compact` is the CPU statement of exactly this arithmetic).
+//
+// Replaces GraphPotential.evaluate = forward + backward_forces (graphnet.py:317-412, 516-537,
+// 567-580) with the TensorNet arithmetic.  Forces come from a hand-written reverse sweep, not
+// autograd; geometry derivatives are collected per directed edge (g_d = dE/dd_e, g_u = dE/du_e)
+// and turned into forces by one gather over each atom's row using the reverse edge, so there is
+// no atomic anywhere in the step and results are bitwise reproducible.
+//
+// Data layout: node tensors are [N][9][C] float32 (irreducible components, channel fastest);
+// a warp owns one node and each lane C/32 consecutive channels, so every row/gather access is a
+// full-width coalesced vector load.  Edges are CSR by receiver, sorted by (receiver, sender).
+// Radial functions (distance projections of the embedding, radial MLP of each layer) are read
+// from per-layer cubic-Hermite tables in u = exp(cutoff_lower - d), built by the host in
+// float64: they depend on the distance only, so tabulating them removes the per-edge MLP
+// (135k MAC/edge/layer) from both the forward and the force pass.
+#include <algorithm>
+
+#include "nnp_common.cuh"
+#include "tn_gemm.cuh"
+#include "tn_math.cuh"
+
+int g_nnp_gemm_use_mma = 1;
+
+namespace {
+
+constexpr float LN_EPS = 1e-5f;
+constexpr float PI_F = 3.14159265358979323846f;
+
+template <int CPL>
+__device__ __forceinline__ void ldv(const float *p, float (&v)[CPL])
+{
+    if constexpr (CPL == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    } else if constexpr (CPL == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+
+template <int CPL>
+__device__ __forceinline__ void stv(float *p, const float (&v)[CPL])
+{
+    if constexpr (CPL == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (CPL == 2) {
+        *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+    } else {
+        p[0] = v[0];
+    }
+}
+
+struct TnDev {
+    nnp_tn_model m;
+    int n, n_samples, capacity;
+    // inputs
+    const int *species, *batch, *order, *row_ptr, *pairs, *nl_counts;
+    const float *deltas, *dists;
+    // outputs
+    float *energy, *forces, *per_atom;
+    // workspace: edges
+    int *col;
+    float4 *geoA;  // (table coordinate, phi, dphi/dd, 1/d)
+    float4 *geoB;  // (ux, uy, uz, u = exp(cutoff_lower - d))
+    float *g_d;
+    float4 *g_u;
+    // workspace: nodes
+    int *zs, *sample_ptr;
+    float *X0, *n0, *ln0, *e0, *e1, *Xm, *Xa, *Xb;
+    float *Xh[NNP_TN_MAX_LAYERS], *nx[NNP_TN_MAX_LAYERS], *Yc[NNP_TN_MAX_LAYERS],
+        *Mc[NNP_TN_MAX_LAYERS], *Dc[NNP_TN_MAX_LAYERS];
+    float *Qc, *lnr, *r0, *r1, *e_atom;
+    float *G1, *G2, *G3;  // [N,9,C] gradient scratch
+    float *g_r1, *g_r0, *g_lnr, *g_e1, *g_e0, *g_ln0;
+};
+
+__device__ __forceinline__ bool overflowed(const TnDev &d)
+{
+    return d.nl_counts != nullptr && d.nl_counts[0] > d.capacity;
+}
+
+// ------------------------------------------------------------------------------- setup
+__global__ void k_prep_nodes(TnDev d)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= d.n) return;
+    const int i = d.order ? d.order[s] : s;
+    d.zs[s] = d.species[i];
+    const int b = d.batch[s];  // batch is in original order; s doubles as an original index here
+    if (s == 0 || d.batch[s - 1] != b) d.sample_ptr[b] = s;
+    if (s == d.n - 1) d.sample_ptr[d.n_samples] = d.n;
+}
+
+// Per-edge geometry shared by every layer of the forward and reverse sweeps.
+// cosine cutoff as radial.py:11-39, u as radial.py:57.
+__global__ void k_edge_geom(TnDev d)
+{
+    if (overflowed(d)) return;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= d.row_ptr[d.n]) return;
+    const int i = d.pairs[2 * (size_t)e], j = d.pairs[2 * (size_t)e + 1];
+    const float dist = d.dists[e];
+    const bool loop = (i == j);
+    const float rl = d.m.cutoff_lower, ru = d.m.cutoff_upper;
+    float phi, dphi;
+    if (rl == 0.0f) {
+        const float x = dist / ru;
+        phi = dist <= ru ? 0.5f * (cospif(x) + 1.0f) : 0.0f;
+        dphi = dist <= ru ? -0.5f * PI_F / ru * sinpif(x) : 0.0f;
+    } else {
+        const float span = ru - rl;
+        const float t = 2.0f * (dist - rl) / span + 1.0f;
+        const bool in = dist >= rl && dist <= ru;
+        phi = in ? 0.5f * (cospif(t) + 1.0f) : 0.0f;
+        dphi = in ? -PI_F / span * sinpif(t) : 0.0f;
+    }
+    const float u = expf(rl - dist);
+    float tx = (u - d.m.u_min) / d.m.u_step;
+    tx = fminf(fmaxf(tx, 0.0f), (float)(d.m.num_knots - 1));
+    const float invd = loop ? 0.0f : 1.0f / dist;
+    d.col[e] = j;
+    d.geoA[e] = make_float4(tx, phi, dphi, invd);
+    d.geoB[e] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
+                            d.deltas[3 * (size_t)e + 2] * invd, u);
+    d.g_d[e] = 0.0f;
+    d.g_u[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Hermite lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coord).
+template <int C, int CPL, bool DERIV>
+__device__ __forceinline__ void table_lookup(const float *__restrict__ tab, int num_knots, float tx,
+                                             int lane, float (&f)[3][CPL], float (&df)[3][CPL])
+{
+    int kn = (int)tx;
+    kn = kn > num_knots - 2 ? num_knots - 2 : kn;
+    const Hermite h = hermite_weights(tx - (float)kn);
+    const float *row0 = tab + (size_t)kn * (6 * C) + lane * CPL;
+    const float *row1 = row0 + 6 * C;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float f0[CPL], m0[CPL], f1[CPL], m1[CPL];
+        ldv<CPL>(row0 + k * C, f0);
+        ldv<CPL>(row0 + (3 + k) * C, m0);
+        ldv<CPL>(row1 + k * C, f1);
+        ldv<CPL>(row1 + (3 + k) * C, m1);
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            f[k][v] = h.h00 * f0[v] + h.h10 * m0[v] + h.h01 * f1[v] + h.h11 * m1[v];
+            if (DERIV) df[k][v] = h.d00 * f0[v] + h.d10 * m0[v] + h.d01 * f1[v] + h.d11 * m1[v];
+        }
+    }
+}
+
+__device__ __forceinline__ int group_of(int q) { return q == 0 ? 0 : (q < 4 ? 1 : 2); }
+
+// ----------------------------------------------------------------------------- embedding
+// X0_i = sum_e w_e[:,grp] * basis_e  with w_e = dp(rho_e) * phi_e * Z_e ; then n0 = |X0|^2 and
+// ln0 = LayerNorm_C(n0).
+template <int C>
+__global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
+{
+    constexpr int CPL = C / 32;
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float zr[CPL];
+    ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
+    float acc[9][CPL];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
+
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int j = d.col[e];
+        const float4 ga = d.geoA[e];
+        const float4 gb = d.geoB[e];
+        float zsnd[CPL];
+        ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
+        float f[3][CPL], df[3][CPL];
+        table_lookup<C, CPL, false>(d.m.tables, d.m.num_knots, ga.x, lane, f, df);
+        float b[9];
+        edge_basis9(gb.x, gb.y, gb.z, b);
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            const float cc = ga.y * (zr[v] + zsnd[v]);
+            const float w0 = f[0][v] * cc, w1 = f[1][v] * cc, w2 = f[2][v] * cc;
+            acc[0][v] += w0;
+#pragma unroll
+            for (int q = 1; q < 4; ++q) acc[q][v] += w1 * b[q];
+#pragma unroll
+            for (int q = 4; q < 9; ++q) acc[q][v] += w2 * b[q];
+        }
+    }
+    float nrm[CPL];
+    float sum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float c9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) c9[q] = acc[q][v];
+        nrm[v] = c9_frob(c9, c9);
+        sum += nrm[v];
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<CPL>(d.X0 + ((size_t)s * 9 + q) * C + cb, acc[q]);
+    stv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+    const float mean = nnp_warp_sum(sum) * (1.0f / C);
+    float var = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) var += (nrm[v] - mean) * (nrm[v] - mean);
+    var = nnp_warp_sum(var) * (1.0f / C);
+    const float rstd = rsqrtf(var + LN_EPS);
+    float g[CPL], bb[CPL], out[CPL];
+    ldv<CPL>(d.m.init_norm_g + cb, g);
+    ldv<CPL>(d.m.init_norm_b + cb, bb);
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) out[v] = (nrm[v] - mean) * rstd * g[v] + bb[v];
+    stv<CPL>(d.ln0 + (size_t)s * C + cb, out);
+}
+
+// ------------------------------------------------------------------------- elementwise
+// one thread per (node, channel); the 9 components are C floats apart
+__device__ __forceinline__ void ld9(const float *base, int C, float *c9)
+{
+#pragma unroll
+    for (int q = 0; q < 9; ++q) c9[q] = base[(size_t)q * C];
+}
+__device__ __forceinline__ void st9(float *base, int C, const float *c9)
+{
+#pragma unroll
+    for (int q = 0; q < 9; ++q) base[(size_t)q * C] = c9[q];
+}
+
+__global__ void k_normalize(const float *__restrict__ X, float *__restrict__ Xh,
+                            float *__restrict__ nx, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float x[9], xh[9];
+    ld9(X + off, C, x);
+    nx[idx] = normalize_fwd(x, xh);
+    st9(Xh + off, C, xh);
+}
+
+__global__ void k_node_product(const float *__restrict__ Mc, const float *__restrict__ Yc,
+                               float *__restrict__ Qc, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float m[9], y[9], q[9];
+    ld9(Mc + off, C, m);
+    ld9(Yc + off, C, y);
+    node_product_fwd(m, y, q);
+    st9(Qc + off, C, q);
+}
+
+__global__ void k_residual(const float *__restrict__ Xh, const float *__restrict__ Dc,
+                           float *__restrict__ Xn, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float xh[9], dc[9], xn[9];
+    ld9(Xh + off, C, xh);
+    ld9(Dc + off, C, dc);
+    residual_fwd(xh, dc, xn);
+    st9(Xn + off, C, xn);
+}
+
+__global__ void k_residual_bwd(const float *__restrict__ G, const float *__restrict__ Dc,
+                               float *__restrict__ GD, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float g[9], dc[9], gd[9];
+    ld9(G + off, C, g);
+    ld9(Dc + off, C, dc);
+    residual_bwd(g, dc, gd);
+    st9(GD + off, C, gd);
+}
+
+__global__ void k_node_product_bwd(const float *__restrict__ Mc, const float *__restrict__ Yc,
+                                   const float *__restrict__ GQ, float *__restrict__ GM,
+                                   float *__restrict__ GY, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float m[9], y[9], gq[9], gm[9], gy[9];
+    ld9(Mc + off, C, m);
+    ld9(Yc + off, C, y);
+    ld9(GQ + off, C, gq);
+    node_product_bwd(m, y, gq, gm, gy);
+    st9(GM + off, C, gm);
+    st9(GY + off, C, gy);
+}
+
+__global__ void k_normalize_bwd(const float *__restrict__ GXh, const float *__restrict__ Xh,
+                                const float *__restrict__ nx, float *__restrict__ GX, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float g[9], xh[9], gx[9];
+    ld9(GXh + off, C, g);
+    ld9(Xh + off, C, xh);
+    normalize_bwd(g, xh, nx[idx], gx);
+    st9(GX + off, C, gx);
+}
+
+// X = Xm * gate[grp], gate = silu(e1):  G_Xm = GX*gate ; g_e1 = <GX, Xm>_grp * silu'(e1)
+__global__ void k_embed_gate_bwd(const float *__restrict__ GX, const float *__restrict__ Xm,
+                                 const float *__restrict__ e1, float *__restrict__ GXm,
+                                 float *__restrict__ g_e1, int n, int C)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * C) return;
+    const int node = idx / C, c = idx - node * C;
+    const size_t off = (size_t)node * 9 * C + c;
+    float g[9], xm[9], gxm[9];
+    ld9(GX + off, C, g);
+    ld9(Xm + off, C, xm);
+    const float *e = e1 + (size_t)node * 3 * C + 3 * c;
+    const float gate[3] = {nnp_silu(e[0]), nnp_silu(e[1]), nnp_silu(e[2])};
+#pragma unroll
+    for (int q = 0; q < 9; ++q) gxm[q] = g[q] * gate[group_of(q)];
+    st9(GXm + off, C, gxm);
+    float *ge = g_e1 + (size_t)node * 3 * C + 3 * c;
+    ge[0] = c9_dot_I(g, xm) * nnp_silu_grad(e[0]);
+    ge[1] = c9_dot_A(g, xm) * nnp_silu_grad(e[1]);
+    ge[2] = c9_dot_S(g, xm) * nnp_silu_grad(e[2]);
+}
+
+// ----------------------------------------------------------------------- interaction edges
+// M_i = sum_e f_e[:,grp] * Yc_j   (f_e = table(u_e) * phi_e)
+template <int C>
+__global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
+{
+    constexpr int CPL = C / 32;
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    const float *Y = d.Yc[layer];
+    float acc[9][CPL];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int j = d.col[e];
+        const float4 ga = d.geoA[e];
+        float f[3][CPL], df[3][CPL];
+        table_lookup<C, CPL, false>(tab, d.m.num_knots, ga.x, lane, f, df);
+        const float *yj = Y + (size_t)j * 9 * C + cb;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            float y[CPL];
+            ldv<CPL>(yj + q * C, y);
+            const int grp = group_of(q);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) acc[q][v] += (f[grp][v] * ga.y) * y[v];
+        }
+    }
+    float *out = d.Mc[layer] + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+// Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
+// is a gather over a's own row):
+//   G_Y[a] += sum_e f_e[:,grp] * G_M[b]              (b = sender of e)
+//   g_d[e] += sum_c sum_k <G_M[a], Yc[b]>_k * d f_e[c,k] / dd
+template <int C>
+__global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
+                                                          float *GY)
+{
+    constexpr int CPL = C / 32;
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    const float *Y = d.Yc[layer];
+    float gma[9][CPL], acc[9][CPL];
+    {
+        const float *p = GM + (size_t)s * 9 * C + cb;
+        const float *py = GY + (size_t)s * 9 * C + cb;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            ldv<CPL>(p + q * C, gma[q]);
+            ldv<CPL>(py + q * C, acc[q]);
+        }
+    }
+    const float inv_step = 1.0f / d.m.u_step;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int j = d.col[e];
+        const float4 ga = d.geoA[e];
+        const float u = d.geoB[e].w;
+        float f[3][CPL], df[3][CPL];
+        table_lookup<C, CPL, true>(tab, d.m.num_knots, ga.x, lane, f, df);
+        const float *gj = GM + (size_t)j * 9 * C + cb;
+        const float *yj = Y + (size_t)j * 9 * C + cb;
+        float gf[3][CPL];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) gf[k][v] = 0.0f;
+        float gmj[9][CPL], yv[9][CPL];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            ldv<CPL>(gj + q * C, gmj[q]);
+            ldv<CPL>(yj + q * C, yv[q]);
+        }
+        float part = 0.0f;
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            float a9[9], y9[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                acc[q][v] += (f[group_of(q)][v] * ga.y) * gmj[q][v];
+                a9[q] = gma[q][v];
+                y9[q] = yv[q][v];
+            }
+            const float gI = c9_dot_I(a9, y9), gA = c9_dot_A(a9, y9), gS = c9_dot_S(a9, y9);
+            // d f_e/dd = phi * d f~/dd + f~ * dphi ;  d f~/dd = -u * (d f~/dt) / u_step
+            const float su = -u * inv_step * ga.y;
+            part += gI * (df[0][v] * su + f[0][v] * ga.z) + gA * (df[1][v] * su + f[1][v] * ga.z) +
+                    gS * (df[2][v] * su + f[2][v] * ga.z);
+        }
+        part = nnp_warp_sum(part);
+        if (lane == 0 && j != s) d.g_d[e] += part;
+    }
+    float *out = GY + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+// --------------------------------------------------------------------------------- readout
+// feats = [|I|^2, |A|^2, |S|^2] -> LayerNorm_{3C}
+template <int C>
+__global__ void __launch_bounds__(256) k_readout_feats(TnDev d, const float *X)
+{
+    constexpr int CPL = C / 32;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float x[9][CPL];
+    const float *p = X + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ldv<CPL>(p + q * C, x[q]);
+    float ft[3][CPL];
+    float sum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float c9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) c9[q] = x[q][v];
+        ft[0][v] = c9_dot_I(c9, c9);
+        ft[1][v] = c9_dot_A(c9, c9);
+        ft[2][v] = c9_dot_S(c9, c9);
+        sum += ft[0][v] + ft[1][v] + ft[2][v];
+    }
+    const float mean = nnp_warp_sum(sum) * (1.0f / (3 * C));
+    float var = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) var += (ft[k][v] - mean) * (ft[k][v] - mean);
+    var = nnp_warp_sum(var) * (1.0f / (3 * C));
+    const float rstd = rsqrtf(var + LN_EPS);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float g[CPL], bb[CPL], out[CPL];
+        ldv<CPL>(d.m.out_norm_g + k * C + cb, g);
+        ldv<CPL>(d.m.out_norm_b + k * C + cb, bb);
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) out[v] = (ft[k][v] - mean) * rstd * g[v] + bb[v];
+        stv<CPL>(d.lnr + (size_t)s * 3 * C + k * C + cb, out);
+    }
+}
+
+// per-atom energy: (silu(r1) . h2_w + h2_b) * std + mean  (graphnet.py:403-406), original order
+__global__ void k_head(TnDev d, int H)
+{
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    float part = 0.0f;
+    for (int h = lane; h < H; h += 32) part += nnp_silu(d.r1[(size_t)s * H + h]) * d.m.h2_w[h];
+    part = nnp_warp_sum(part);
+    if (lane == 0) {
+        const float e = (part + d.m.h2_b) * d.m.std + d.m.mean;
+        d.e_atom[d.order ? d.order[s] : s] = e;
+    }
+}
+
+// per-sample sums in float64, fixed order (graphnet.py:411 segment_sum over batch)
+__global__ void __launch_bounds__(256) k_energy_sum(TnDev d)
+{
+    const int b = blockIdx.x;
+    const int p0 = d.sample_ptr[b], p1 = d.sample_ptr[b + 1];
+    double acc = 0.0;
+    for (int i = p0 + threadIdx.x; i < p1; i += blockDim.x) acc += (double)d.e_atom[i];
+    __shared__ double sh[8];
+    acc = nnp_warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sh[w];
+        d.energy[b] = (float)t;
+    }
+}
+
+__global__ void k_copy_per_atom(TnDev d)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < d.n) d.per_atom[i] = d.e_atom[i];
+}
+
+__global__ void k_head_bwd(TnDev d, int H)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= d.n * H) return;
+    const int h = idx % H;
+    d.g_r1[idx] = d.m.std * d.m.h2_w[h] * nnp_silu_grad(d.r1[idx]);
+}
+
+// reverse of k_readout_feats: GX = 2 * g_feats[grp] * X_part
+template <int C>
+__global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, float *GX)
+{
+    constexpr int CPL = C / 32;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float x[9][CPL];
+    const float *p = X + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ldv<CPL>(p + q * C, x[q]);
+    float ft[3][CPL];
+    float sum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float c9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) c9[q] = x[q][v];
+        ft[0][v] = c9_dot_I(c9, c9);
+        ft[1][v] = c9_dot_A(c9, c9);
+        ft[2][v] = c9_dot_S(c9, c9);
+        sum += ft[0][v] + ft[1][v] + ft[2][v];
+    }
+    const float inv_n = 1.0f / (3 * C);
+    const float mean = nnp_warp_sum(sum) * inv_n;
+    float var = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) var += (ft[k][v] - mean) * (ft[k][v] - mean);
+    var = nnp_warp_sum(var) * inv_n;
+    const float rstd = rsqrtf(var + LN_EPS);
+    float gxh[3][CPL], xh[3][CPL];
+    float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float g[CPL], gy[CPL];
+        ldv<CPL>(d.m.out_norm_g + k * C + cb, g);
+        ldv<CPL>(d.g_lnr + (size_t)s * 3 * C + k * C + cb, gy);
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            xh[k][v] = (ft[k][v] - mean) * rstd;
+            gxh[k][v] = gy[v] * g[v];
+            s1 += gxh[k][v];
+            s2 += gxh[k][v] * xh[k][v];
+        }
+    }
+    s1 = nnp_warp_sum(s1) * inv_n;
+    s2 = nnp_warp_sum(s2) * inv_n;
+    float *out = GX + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        const int k = group_of(q);
+        float o[CPL];
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            const float gf = rstd * (gxh[k][v] - s1 - xh[k][v] * s2);
+            o[v] = 2.0f * gf * x[q][v];
+        }
+        stv<CPL>(out + q * C, o);
+    }
+}
+
+// G_X0 = G_X0part + 2 * g_n0 * X0, g_n0 = LayerNorm_C backward of g_ln0
+template <int C>
+__global__ void __launch_bounds__(256) k_embed_norm_bwd(TnDev d, float *GX0)
+{
+    constexpr int CPL = C / 32;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float nrm[CPL], g[CPL], gy[CPL];
+    ldv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+    ldv<CPL>(d.m.init_norm_g + cb, g);
+    ldv<CPL>(d.g_ln0 + (size_t)s * C + cb, gy);
+    float sum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) sum += nrm[v];
+    const float mean = nnp_warp_sum(sum) * (1.0f / C);
+    float var = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) var += (nrm[v] - mean) * (nrm[v] - mean);
+    var = nnp_warp_sum(var) * (1.0f / C);
+    const float rstd = rsqrtf(var + LN_EPS);
+    float xh[CPL], gxh[CPL];
+    float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        xh[v] = (nrm[v] - mean) * rstd;
+        gxh[v] = gy[v] * g[v];
+        s1 += gxh[v];
+        s2 += gxh[v] * xh[v];
+    }
+    s1 = nnp_warp_sum(s1) * (1.0f / C);
+    s2 = nnp_warp_sum(s2) * (1.0f / C);
+    float gn[CPL];
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) gn[v] = rstd * (gxh[v] - s1 - xh[v] * s2);
+    const float *x0 = d.X0 + (size_t)s * 9 * C + cb;
+    float *out = GX0 + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        float x[CPL], o[CPL];
+        ldv<CPL>(x0 + q * C, x);
+        ldv<CPL>(out + q * C, o);
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) o[v] += 2.0f * gn[v] * x[v];
+        stv<CPL>(out + q * C, o);
+    }
+}
+
+// reverse of k_embed_edge: per edge g_d += dE/dd (through dp(rho) and phi) and g_u = dE/du
+template <int C>
+__global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX0)
+{
+    constexpr int CPL = C / 32;
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float zr[CPL];
+    ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
+    float G[9][CPL];
+    const float *p = GX0 + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ldv<CPL>(p + q * C, G[q]);
+    const float inv_step = 1.0f / d.m.u_step;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int j = d.col[e];
+        if (j == s) continue;  // a self loop has no geometry
+        const float4 ga = d.geoA[e];
+        const float4 gb = d.geoB[e];
+        float zsnd[CPL];
+        ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
+        float f[3][CPL], df[3][CPL];
+        table_lookup<C, CPL, true>(d.m.tables, d.m.num_knots, ga.x, lane, f, df);
+        float b[9];
+        edge_basis9(gb.x, gb.y, gb.z, b);
+        const float su = -gb.w * inv_step * ga.y;
+        float pd = 0.0f, px = 0.0f, py = 0.0f, pz = 0.0f;
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) {
+            const float Z = zr[v] + zsnd[v];
+            float g9[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) g9[q] = G[q][v];
+            const float gw0 = 3.0f * g9[0];
+            const float gw1 = 2.0f * (g9[1] * b[1] + g9[2] * b[2] + g9[3] * b[3]);
+            const float gw2 = c9_dot_S(g9, b);
+            pd += Z * (gw0 * (df[0][v] * su + f[0][v] * ga.z) + gw1 * (df[1][v] * su + f[1][v] * ga.z) +
+                       gw2 * (df[2][v] * su + f[2][v] * ga.z));
+            const float w1 = f[1][v] * ga.y * Z, w2 = f[2][v] * ga.y * Z;
+            const float szz = -g9[4] - g9[5];
+            px += 2.0f * (w1 * g9[1] + w2 * (g9[4] * gb.x + g9[6] * gb.y + g9[7] * gb.z));
+            py += 2.0f * (w1 * g9[2] + w2 * (g9[6] * gb.x + g9[5] * gb.y + g9[8] * gb.z));
+            pz += 2.0f * (w1 * g9[3] + w2 * (g9[7] * gb.x + g9[8] * gb.y + szz * gb.z));
+        }
+        pd = nnp_warp_sum(pd);
+        px = nnp_warp_sum(px);
+        py = nnp_warp_sum(py);
+        pz = nnp_warp_sum(pz);
+        if (lane == 0) {
+            d.g_d[e] += pd;
+            d.g_u[e] = make_float4(px, py, pz, 0.0f);
+        }
+    }
+}
+
+// forces: F_i = -sum_{e in row i} [ (g_d[e] + g_d[e']) u_e + (1 - u u^T)(g_u[e] - g_u[e']) / d_e ]
+// with e' the reverse edge (u_e' = -u_e), found by bisection in the sender's sorted row.
+__global__ void k_forces(TnDev d)
+{
+    if (overflowed(d)) return;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= d.n) return;
+    float gx = 0.0f, gy = 0.0f, gz = 0.0f;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0; e < e1; ++e) {
+        const int j = d.col[e];
+        if (j == s) continue;
+        int lo = d.row_ptr[j], hi = d.row_ptr[j + 1] - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (d.col[mid] < s) lo = mid + 1; else hi = mid;
+        }
+        const int er = lo;
+        const float4 ga = d.geoA[e];
+        const float4 gb = d.geoB[e];
+        const float4 ue = d.g_u[e], ur = d.g_u[er];
+        const float gd = d.g_d[e] + d.g_d[er];
+        const float vx = ue.x - ur.x, vy = ue.y - ur.y, vz = ue.z - ur.z;
+        const float dot = vx * gb.x + vy * gb.y + vz * gb.z;
+        gx += gd * gb.x + (vx - gb.x * dot) * ga.w;
+        gy += gd * gb.y + (vy - gb.y * dot) * ga.w;
+        gz += gd * gb.z + (vz - gb.z * dot) * ga.w;
+    }
+    const size_t o = 3 * (size_t)(d.order ? d.order[s] : s);
+    d.forces[o] = -gx;
+    d.forces[o + 1] = -gy;
+    d.forces[o + 2] = -gz;
+}
+
+__global__ void k_fill_int(int *p, int n, int v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// --------------------------------------------------------------------------------- host side
+size_t carve(TnDev &d, void *ws)
+{
+    NnpArena ar(ws);
+    const size_t n = (size_t)d.n, C = (size_t)d.m.channels, cap = (size_t)d.capacity;
+    const size_t T = n * 9 * C;
+    const int L = d.m.num_layers;
+    d.col = ar.take<int>(cap);
+    d.geoA = ar.take<float4>(cap);
+    d.geoB = ar.take<float4>(cap);
+    d.g_d = ar.take<float>(cap);
+    d.g_u = ar.take<float4>(cap);
+    d.zs = ar.take<int>(n);
+    d.sample_ptr = ar.take<int>((size_t)d.n_samples + 1);
+    d.X0 = ar.take<float>(T);
+    d.n0 = ar.take<float>(n * C);
+    d.ln0 = ar.take<float>(n * C);
+    d.e0 = ar.take<float>(n * 2 * C);
+    d.e1 = ar.take<float>(n * 3 * C);
+    d.Xm = ar.take<float>(T);
+    d.Xa = ar.take<float>(T);
+    d.Xb = ar.take<float>(T);
+    for (int l = 0; l < L; ++l) {
+        d.Xh[l] = ar.take<float>(T);
+        d.nx[l] = ar.take<float>(n * C);
+        d.Yc[l] = ar.take<float>(T);
+        d.Mc[l] = ar.take<float>(T);
+        d.Dc[l] = ar.take<float>(T);
+    }
+    d.Qc = ar.take<float>(T);
+    d.lnr = ar.take<float>(n * 3 * C);
+    d.r0 = ar.take<float>(n * C);
+    d.r1 = ar.take<float>(n * (C / 2));
+    d.e_atom = ar.take<float>(n);
+    d.G1 = ar.take<float>(T);
+    d.G2 = ar.take<float>(T);
+    d.G3 = ar.take<float>(T);
+    d.g_r1 = ar.take<float>(n * (C / 2));
+    d.g_r0 = ar.take<float>(n * C);
+    d.g_lnr = ar.take<float>(n * 3 * C);
+    d.g_e1 = ar.take<float>(n * 3 * C);
+    d.g_e0 = ar.take<float>(n * 2 * C);
+    d.g_ln0 = ar.take<float>(n * C);
+    return ar.bytes();
+}
+
+int validate_model(const nnp_tn_model *m)
+{
+    NNP_CHECK_ARG(m != nullptr, "model is NULL");
+    NNP_CHECK_ARG(m->channels == 32 || m->channels == 64 || m->channels == 128,
+                  "channels must be 32, 64 or 128");
+    NNP_CHECK_ARG(m->num_layers >= 0 && m->num_layers <= NNP_TN_MAX_LAYERS, "num_layers out of range");
+    NNP_CHECK_ARG(m->num_knots >= 2, "num_knots must be >= 2");
+    NNP_CHECK_ARG(m->u_step > 0.0f, "u_step must be positive");
+    NNP_CHECK_ARG(m->cutoff_lower >= 0.0f && m->cutoff_lower < m->cutoff_upper, "bad cutoffs");
+    return NNP_OK;
+}
+
+GemmArgs plain_gemm(const float *A, const float *W, const float *bias, float *out, int M, int N,
+                    int K, const float *aux = nullptr, int ldaux = 0)
+{
+    GemmArgs g{};
+    g.A = A;
+    g.W = W;
+    g.bias = bias;
+    g.out = out;
+    g.aux = aux;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.lda = K;
+    g.ldo = N;
+    g.ldaux = ldaux;
+    return g;
+}
+
+// the three component groups (I: 1 comp, A: 3, S: 5) of a [N,9,C] tensor against W[3][C][C]
+GemmBatch mix_gemm(const float *A, const float *W3, float *out, int n, int C, float *out2 = nullptr,
+                   const float *aux = nullptr, int ldaux = 0)
+{
+    static const int ncomp[3] = {1, 3, 5}, q0[3] = {0, 1, 4};
+    GemmBatch b{};
+    for (int k = 0; k < 3; ++k) {
+        GemmArgs &g = b.g[k];
+        g.A = A;
+        g.W = W3 + (size_t)k * C * C;
+        g.out = out;
+        g.out2 = out2;
+        g.aux = aux;
+        g.M = n * ncomp[k];
+        g.N = C;
+        g.K = C;
+        g.lda = C;
+        g.ldo = C;
+        g.ldaux = ldaux;
+        g.ncomp = ncomp[k];
+        g.q0 = q0[k];
+        g.grp = k;
+    }
+    return b;
+}
+
+template <int C>
+int run_step(TnDev &d, cudaStream_t st)
+{
+    const int n = d.n, L = d.m.num_layers, H = C / 2;
+    const int warp_blocks = nnp_blocks(n, 8);
+    const int ew_blocks = nnp_blocks((int64_t)n * C, 256);
+    const nnp_tn_model &m = d.m;
+    int rc;
+#define RUN(x)            \
+    do {                  \
+        rc = (x);         \
+        if (rc) return rc; \
+    } while (0)
+
+    k_fill_int<<<nnp_blocks(d.n_samples + 1, 256), 256, 0, st>>>(d.sample_ptr, d.n_samples + 1, n);
+    k_prep_nodes<<<nnp_blocks(n, 256), 256, 0, st>>>(d);
+    k_edge_geom<<<nnp_blocks(d.capacity, 256), 256, 0, st>>>(d);
+
+    // ---- embedding
+    k_embed_edge<C><<<warp_blocks, 256, 0, st>>>(d);
+    {
+        GemmBatch b{};
+        b.g[0] = plain_gemm(d.ln0, m.es0_w, m.es0_b, d.e0, n, 2 * C, C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        b.g[0] = plain_gemm(d.e0, m.es1_w, m.es1_b, d.e1, n, 3 * C, 2 * C);
+        RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st)));
+        GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xa, n, C, d.Xm, d.e1, 3 * C);
+        RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st)));
+    }
+    float *X = d.Xa, *Xother = d.Xb;
+
+    // ---- interaction layers
+    for (int l = 0; l < L; ++l) {
+        k_normalize<<<ew_blocks, 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C);
+        GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st)));
+        k_edge_message<C><<<warp_blocks, 256, 0, st>>>(d, l);
+        k_node_product<<<ew_blocks, 256, 0, st>>>(d.Mc[l], d.Yc[l], d.Qc, n, C);
+        GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + (size_t)3 * C * C, d.Dc[l], n, C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st)));
+        k_residual<<<ew_blocks, 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, n, C);
+        std::swap(X, Xother);
+    }
+
+    // ---- readout
+    k_readout_feats<C><<<warp_blocks, 256, 0, st>>>(d, X);
+    {
+        GemmBatch b{};
+        b.g[0] = plain_gemm(d.lnr, m.lin_w, m.lin_b, d.r0, n, C, 3 * C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        b.g[0] = plain_gemm(d.r0, m.h1_w, m.h1_b, d.r1, n, H, C);
+        RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st)));
+    }
+    k_head<<<warp_blocks, 256, 0, st>>>(d, H);
+    k_energy_sum<<<d.n_samples, 256, 0, st>>>(d);
+    if (d.per_atom) k_copy_per_atom<<<nnp_blocks(n, 256), 256, 0, st>>>(d);
+    NNP_CHECK_LAUNCH("tensornet forward");
+    if (!d.forces) return NNP_OK;
+
+    // ================================================================= reverse sweep
+    k_head_bwd<<<nnp_blocks((int64_t)n * H, 256), 256, 0, st>>>(d, H);
+    {
+        GemmBatch b{};
+        // g_r0 = (g_r1 @ h1_w) * silu'(r0)
+        b.g[0] = plain_gemm(d.g_r1, m.h1_wT, nullptr, d.g_r0, n, C, H, d.r0, C);
+        RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st)));
+        b.g[0] = plain_gemm(d.g_r0, m.lin_wT, nullptr, d.g_lnr, n, 3 * C, C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+    }
+    float *GX = d.G1, *Ga = d.G2, *Gb = d.G3;
+    k_readout_bwd<C><<<warp_blocks, 256, 0, st>>>(d, X, GX);
+
+    for (int l = L - 1; l >= 0; --l) {
+        // GX = dL/dX_{l+1}.  dL/dXh starts as GX itself.
+        k_residual_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Dc[l], Ga, n, C);              // Ga = G_D
+        GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + (size_t)3 * C * C, Gb, n, C);     // Gb = G_Q
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st)));
+        k_node_product_bwd<<<ew_blocks, 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C);
+        // now Ga = G_M, Qc = G_Y (local part)
+        k_edge_message_bwd<C><<<warp_blocks, 256, 0, st>>>(d, l, Ga, d.Qc);
+        // G_Xh = GX + mix^T(G_Y)  -> written in place over GX
+        GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GX, n, C, nullptr, GX, C);
+        RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st)));
+        k_normalize_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Xh[l], d.nx[l], Gb, n, C);
+        std::swap(GX, Gb);
+    }
+
+    // ---- embedding reverse: X = Xm * gate
+    k_embed_gate_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Xm, d.e1, Ga, d.g_e1, n, C);     // Ga = G_Xm
+    {
+        GemmBatch b{};
+        b.g[0] = plain_gemm(d.g_e1, m.es1_wT, nullptr, d.g_e0, n, 2 * C, 3 * C, d.e0, 2 * C);
+        RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st)));
+        b.g[0] = plain_gemm(d.g_e0, m.es0_wT, nullptr, d.g_ln0, n, C, 2 * C);
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        GemmBatch mx = mix_gemm(Ga, m.et_wT, Gb, n, C);                                 // Gb = G_X0 part
+        RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st)));
+    }
+    k_embed_norm_bwd<C><<<warp_blocks, 256, 0, st>>>(d, Gb);
+    k_embed_edge_bwd<C><<<warp_blocks, 256, 0, st>>>(d, Gb);
+    k_forces<<<nnp_blocks(n, 128), 128, 0, st>>>(d);
+    NNP_CHECK_LAUNCH("tensornet reverse");
+#undef RUN
+    return NNP_OK;
+}
+
+__global__ void k_identity(const float *in, float *out, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+}
+
+}  // namespace
+
+extern "C" int nnp_tn_workspace_bytes(const nnp_tn_model *m, int32_t n_atoms, int32_t capacity,
+                                      int32_t n_samples, size_t *bytes)
+{
+    int rc = validate_model(m);
+    if (rc) return rc;
+    NNP_CHECK_ARG(n_atoms >= 1 && capacity >= 1 && n_samples >= 1 && bytes, "bad sizes");
+    TnDev d{};
+    d.m = *m;
+    d.n = n_atoms;
+    d.capacity = capacity;
+    d.n_samples = n_samples;
+    *bytes = carve(d, nullptr);
+    return NNP_OK;
+}
+
+extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_samples,
+                                    int32_t capacity, const int32_t *species, const int32_t *batch,
+                                    const int32_t *order, const int32_t *row_ptr,
+                                    const int32_t *pairs, const float *deltas, const float *dists,
+                                    const int32_t *nl_counts, float *energy, float *forces,
+                                    float *per_atom, void *workspace, size_t workspace_bytes,
+                                    nnp_stream_t stream)
+{
+    int rc = validate_model(m);
+    if (rc) return rc;
+    NNP_CHECK_ARG(n_atoms >= 1 && capacity >= 1 && n_samples >= 1, "bad sizes");
+    NNP_CHECK_ARG(species && batch && row_ptr && pairs && deltas && dists && energy && workspace,
+                  "NULL buffer passed to nnp_tn_energy_forces");
+    TnDev d{};
+    d.m = *m;
+    d.n = n_atoms;
+    d.capacity = capacity;
+    d.n_samples = n_samples;
+    size_t need = carve(d, workspace);
+    if (need > workspace_bytes) {
+        nnp_set_error("workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+        return NNP_ERR_WORKSPACE;
+    }
+    d.species = species;
+    d.batch = batch;
+    d.order = order;
+    d.row_ptr = row_ptr;
+    d.pairs = pairs;
+    d.deltas = deltas;
+    d.dists = dists;
+    d.nl_counts = nl_counts;
+    d.energy = energy;
+    d.forces = forces;
+    d.per_atom = per_atom;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (m->channels) {
+    case 32: return run_step<32>(d, st);
+    case 64: return run_step<64>(d, st);
+    default: return run_step<128>(d, st);
+    }
+}
+
+extern "C" int nnp_set_gemm_mode(int use_mma)
+{
+    g_nnp_gemm_use_mma = use_mma ? 1 : 0;
+    return NNP_OK;
+}
+
+extern "C" int nnp_test_gemm_nt(const float *A, const float *W, const float *bias, float *out,
+                                int32_t M, int32_t N, int32_t K, nnp_stream_t stream)
+{
+    NNP_CHECK_ARG(A && W && out && M >= 1 && N >= 1 && K >= 4, "bad arguments to nnp_test_gemm_nt");
+    GemmBatch b{};
+    b.g[0] = plain_gemm(A, W, bias, out, M, N, K);
+    return gemm_launch<PRO_NONE, EPI_STORE>(b, 1, static_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,241 @@
+"""Parity of the CUDA TensorNet step (through the C ABI) with the float64 CPU oracle.
+
+Tolerances are the north star's: per-sample energy |E_gpu - E_ref| / max(|E_ref|, 1) <= 1e-5,
+forces max|F_gpu - F_ref| / max|F_ref| <= 1e-4 (FP32 on the device, float64 oracle).
+The oracle itself is parity-unpinned (no reference TensorNet exists; see its header).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import torch  # noqa: E402
+
+from oracle import neighbors_oracle as O  # noqa: E402
+from oracle import tensornet_oracle as T  # noqa: E402
+
+import paper_2402_17660_b200 as P  # noqa: E402
+from paper_2402_17660_b200 import _lib, synth  # noqa: E402
+
+E_TOL = 1e-5
+F_TOL = 1e-4
+
+
+def oracle_eval(model, z, pos, batch, box, forces=True):
+    cfg = model.config
+    ocfg = T.OracleConfig(cfg.embedding_dimension, cfg.num_layers, cfg.num_rbf, cfg.cutoff_lower,
+                          cfg.cutoff_upper, cfg.max_z, cfg.mean, cfg.std)
+    n = len(pos)
+    nl = O.build_with_auto_capacity(pos, batch, box, cfg.cutoff_upper, 64 * n,
+                                    cutoff_lower=cfg.cutoff_lower,
+                                    strategy="cell" if n > 3000 else "brute",
+                                    full_list=True, include_self_loops=True)
+    pr, dl, ds = nl.valid()
+    return T.energy_forces_compact(model.params, ocfg, z, batch, pr, dl, ds, want_forces=forces)
+
+
+def check(model, z, pos, batch, box, e_tol=E_TOL, f_tol=F_TOL):
+    e, f = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32),
+                 None if batch is None else torch.as_tensor(batch), box)
+    b = np.zeros(len(pos), dtype=np.int64) if batch is None else batch
+    e_ref, f_ref, _ = oracle_eval(model, z, pos, b, box)
+    e_err = np.max(np.abs(e.cpu().numpy() - e_ref) / np.maximum(np.abs(e_ref), 1.0))
+    f_err = np.max(np.abs(f.cpu().numpy() - f_ref)) / np.max(np.abs(f_ref))
+    assert e_err <= e_tol, f"energy rel err {e_err:.3e}"
+    assert f_err <= f_tol, f"force rel err {f_err:.3e}"
+    return e_err, f_err
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_gemm_tile_engine(mode):
+    lib = _lib.load()
+    lib.nnp_set_gemm_mode(mode)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(0)
+        for M, N, K in [(64, 64, 32), (200, 128, 128), (333, 384, 256), (70, 16, 64), (129, 96, 16)]:
+            A = torch.randn(M, K, device="cuda", generator=g)
+            W = torch.randn(N, K, device="cuda", generator=g)
+            bias = torch.randn(N, device="cuda", generator=g)
+            out = torch.empty(M, N, device="cuda")
+            rc = lib.nnp_test_gemm_nt(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(),
+                                      M, N, K, torch.cuda.current_stream().cuda_stream)
+            assert rc == 0
+            ref = (A.double() @ W.double().T + bias.double())
+            err = (out.double() - ref).abs().max().item() / ref.abs().max().item()
+            assert err < 2e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
+    finally:
+        lib.nnp_set_gemm_mode(1)
+
+
+def small_open(rng, n=20):
+    pos = rng.uniform(0, 5.0, (n, 3)).astype(np.float32).astype(np.float64)
+    z = rng.choice([1, 6, 7, 8], n)
+    batch = np.repeat([0, 1], [n - n // 2, n // 2])
+    return z, pos, batch, None
+
+
+@pytest.mark.parametrize("C", [32, 64, 128])
+@pytest.mark.parametrize("L", [0, 1, 2])
+def test_small_open_system(rng, C, L):
+    model = P.TensorNet(embedding_dimension=C, num_layers=L, num_rbf=16, cutoff_upper=4.0,
+                        max_z=10, mean=0.3, std=1.7, seed=3)
+    assert model.table_error < 1e-6
+    check(model, *small_open(rng))
+
+
+@pytest.mark.parametrize("gemm_mode", [1, 0])
+def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
+    _lib.load().nnp_set_gemm_mode(gemm_mode)
+    try:
+        box = np.array([[11.0, 0, 0], [2.5, 10.5, 0], [-3.0, 1.5, 12.0]])
+        pos = (rng.uniform(0, 1, (90, 3)) @ box).astype(np.float32).astype(np.float64)
+        z = rng.choice([1, 6, 8], 90)
+        model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.5,
+                            max_z=10, seed=5)
+        check(model, z, pos, None, box)
+        model = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_lower=0.7,
+                            cutoff_upper=4.5, max_z=10, seed=6)
+        check(model, z, pos, None, box)
+    finally:
+        _lib.load().nnp_set_gemm_mode(1)
+
+
+def test_config_a_alanine_sized_molecule():
+    z, pos, batch, box = synth.config_a_molecule()
+    model = P.TensorNet(embedding_dimension=128, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=0)
+    check(model, z, pos, None, None)
+
+
+def test_cell_path_with_renumbering_medium_periodic():
+    """3 000 atoms at water density: cell strategy, cell-sorted internal numbering."""
+    z, pos, batch, box = synth.config_c_box(n=3000, edge=31.0, seed=7)
+    model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=16, cutoff_upper=5.0,
+                        max_z=10, seed=1, strategy="cell")
+    check(model, z, pos, None, box)
+    brute = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=16, cutoff_upper=5.0,
+                        max_z=10, seed=1, strategy="brute")
+    e1, f1 = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), None, box)
+    e2, f2 = brute(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), None, box)
+    assert abs(float(e1[0] - e2[0])) / max(abs(float(e2[0])), 1.0) < 1e-5
+    assert float((f1 - f2).abs().max() / f2.abs().max()) < 1e-4
+
+
+def test_batched_molecules():
+    z, pos, batch, _ = synth.config_d_molecules(64, seed=4)
+    model = P.TensorNet(embedding_dimension=64, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=2)
+    check(model, z, pos, batch, None)
+    # batch independence: a slice of samples gives the same numbers
+    sel = batch < 8
+    e_all, f_all = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    e_sub, f_sub = model(torch.as_tensor(z[sel]), torch.as_tensor(pos[sel], dtype=torch.float32),
+                         torch.as_tensor(batch[sel]))
+    assert torch.allclose(e_all[:8], e_sub, rtol=1e-6, atol=1e-6)
+    assert torch.allclose(f_all[: int(sel.sum())], f_sub, rtol=1e-5, atol=1e-7)
+
+
+def test_graph_replay_equals_eager_and_is_deterministic(rng):
+    z, pos, batch, _ = small_open(rng, 30)
+    args = (torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    a = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)
+    b = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1,
+                    use_graph=False)
+    e1, f1 = a(*args)
+    e2, f2 = a(*args)          # second call replays the captured graph
+    e3, f3 = b(*args)
+    assert torch.equal(e1, e2) and torch.equal(f1, f2)
+    assert torch.equal(e1, e3) and torch.equal(f1, f3)
+
+
+def test_overflow_grows_capacity(rng):
+    z, pos, batch, _ = small_open(rng, 40)
+    tight = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10,
+                        seed=1, max_num_neighbors=1)
+    roomy = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)
+    args = (torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    e1, f1 = tight(*args)
+    e2, f2 = roomy(*args)
+    assert torch.equal(e1, e2) and torch.equal(f1, f2)
+
+
+def test_evaluate_call_shapes_and_validation(rng):
+    z, pos, batch, _ = small_open(rng, 24)
+    model = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)
+    system = P.build_system(pos, z, batch=batch)
+    pot = P.ComposedPotential(network=model)
+    res = P.evaluate_auto(pot, system)
+    e, f = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    assert np.allclose(res.energy, e.cpu().numpy(), rtol=1e-6, atol=1e-6)
+    assert np.allclose(res.forces, f.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    assert np.allclose(np.bincount(batch, weights=res.per_atom_energy), res.energy, rtol=1e-5)
+    half = P.build_neighbor_list(system, P.NeighborSpec(cutoff_upper=4.0, capacity=2000))
+    with pytest.raises(P.ValidationError, match="full neighbor list"):
+        model.evaluate(system, half)
+    other = P.build_neighbor_list(system, P.NeighborSpec(cutoff_upper=3.0, capacity=2000, full_list=True,
+                                                         include_self_loops=True))
+    with pytest.raises(P.ValidationError, match="cutoff mismatch"):
+        model.evaluate(system, other)
+    with pytest.raises(P.ValidationError, match="out of range"):
+        model.evaluate(P.build_system(pos, np.full(len(pos), 11), batch=batch))
+
+
+def test_invariances_on_device(rng):
+    z, pos, batch, _ = small_open(rng, 26)
+    model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=2)
+    e0, f0 = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    pos2 = pos @ (-q).T + np.array([1.5, -0.7, 2.2])           # improper rotation + shift
+    e1, f1 = model(torch.as_tensor(z), torch.as_tensor(pos2, dtype=torch.float32), torch.as_tensor(batch))
+    assert np.max(np.abs((e1 - e0).cpu().numpy()) / np.maximum(np.abs(e0.cpu().numpy()), 1.0)) < 2e-5
+    fr = f0.cpu().numpy() @ (-q).T
+    assert np.max(np.abs(f1.cpu().numpy() - fr)) / np.max(np.abs(fr)) < 5e-4
+    # net force vanishes (translation invariance)
+    assert float(f0.sum(0).abs().max()) < 1e-4 * float(f0.abs().max()) * len(pos)
+
+
+def test_cell_path_full_model_forces_medium_periodic():
+    """1 500 atoms at config-C density, full-size model (128 channels, 2 layers), cell strategy:
+    energy and forces against the float64 oracle (the oracle needs ~30 s here)."""
+    z, pos, batch, box = synth.config_c_box(n=1500, edge=24.85, seed=11)
+    model = P.TensorNet(embedding_dimension=128, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=0,
+                        strategy="cell")
+    check(model, z, pos, None, box)
+
+
+def test_config_c_full_size_properties():
+    """23 558 atoms, 2 layers, 128 channels: finite, deterministic, zero net force, per-atom
+    energies sum to the sample energy, and per-atom energies of the atoms at the centre of the
+    box equal the oracle's on the sub-system inside their receptive field ((L+1) * r_u = 15 A;
+    the float64 oracle on the whole box would take minutes)."""
+    z, pos, batch, box = synth.config_c_box()
+    n = len(pos)
+    model = P.TensorNet(embedding_dimension=128, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=0)
+    zt, pt = torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32)
+    e1, f1 = model(zt, pt, None, box)
+    per_atom = model.last_per_atom_energy(n).cpu().numpy().astype(np.float64)
+    e2, f2 = model(zt, pt, None, box)
+    assert torch.isfinite(e1).all() and torch.isfinite(f1).all()
+    assert torch.equal(e1, e2) and torch.equal(f1, f2)
+    assert float(f1.sum(0).abs().max()) < 1e-3 * float(f1.abs().max()) * 50
+    assert abs(per_atom.sum() - float(e1[0])) / abs(float(e1[0])) < 1e-6
+    edge = box[0, 0]
+    centre = np.full(3, edge / 2)
+    d = pos - centre
+    d -= edge * np.rint(d / edge)
+    r = np.linalg.norm(d, axis=1)
+    sub = np.where(r <= 17.0)[0]
+    inner = np.where(r[sub] <= 2.0)[0]
+    assert len(inner) >= 2
+    cfg = model.config
+    ocfg = T.OracleConfig(cfg.embedding_dimension, cfg.num_layers, cfg.num_rbf, cfg.cutoff_lower,
+                          cfg.cutoff_upper, cfg.max_z, cfg.mean, cfg.std)
+    sp = centre + d[sub]
+    nl = O.build_neighbor_list(sp, None, None, 5.0, 80 * len(sub), strategy="cell", full_list=True,
+                               include_self_loops=True)
+    pr, dl, ds = nl.valid()
+    _, _, pa_ref = T.energy_forces_compact(model.params, ocfg, z[sub], np.zeros(len(sub), np.int64),
+                                           pr, dl, ds, want_forces=False)
+    err = np.max(np.abs(per_atom[sub[inner]] - pa_ref[inner]))
+    assert err < 5e-6, f"per-atom energy error {err:.3e}"
