@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: TensorNet energy+forces steps/s (neighbor search included).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C|A|D|E] [--no-sweep] [--no-cpu]
+
+A "step" is one pass of the hot path over one batch of synthetic input: cutoff neighbor
+search (cell list) + TensorNet forward + analytic force sweep, replayed as one CUDA graph.
+Default workload = BASELINE.json configs[2]: 2-layer, 128-channel TensorNet on the synthetic
+23,558-atom periodic box (the configuration the north-star target is quoted on).  With
+N > 1 the box does not shard ("replicas only"), so every rank steps its own
+replica ("weak" scaling); `--workload D` shards 8192 molecules by whole molecules instead.
+
+One JSON line on stdout (rank 0).  `value` = whole-job steps/s with inputs resident in HBM;
+`e2e` = the same through TensorNet.forward with pinned HOST buffers (H2D of species+positions
+and D2H of energy+forces inside the timed region).  `--impl reference` times the CPU oracle
+port (there is no compilable reference: the reference is Python/numba) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TensorNet energy+forces steps/s (neighbor search included)"
+CHANNELS, LAYERS, NUM_RBF, CUTOFF = 128, 2, 32, 5.0
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload(name: str, rank: int = 0, world: int = 1):
+    from paper_2402_17660_b200 import synth
+
+    if name == "A":
+        z, pos, batch, box = synth.config_a_molecule()
+        desc = "A: 22-atom molecule, open boundaries"
+    elif name == "C":
+        z, pos, batch, box = synth.config_c_box()
+        desc = "C: 23,558-atom periodic cubic box (62.23 A), water-like species"
+    elif name == "D":
+        z, pos, batch, box = synth.config_d_molecules(8192)
+        shards = synth.shard_by_molecule(batch, world)
+        a0, a1, s0, _ = shards[rank]
+        z, pos, batch = z[a0:a1], pos[a0:a1], batch[a0:a1] - s0
+        desc = f"D: 8192 QM9-sized molecules sharded by molecule over {world} rank(s)"
+    elif name == "E":
+        z, pos, batch, box = synth.config_e_triclinic()
+        desc = "E: 100,000-atom triclinic periodic water box"
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return z, pos, batch, box, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def algorithmic_bytes(n_atoms: int, n_edges: int, n_cells: int):
+    """Compulsory HBM bytes; gathers counted once per pass."""
+    T = 9 * CHANNELS * 4
+    L = LAYERS
+    per_kernel = {
+        "k_edge_message": 2 * T * n_atoms + 20 * n_edges,
+        "k_edge_message_bwd": 4 * T * n_atoms + 44 * n_edges,
+        "k_embed_edge": T * n_atoms + 8 * CHANNELS * n_atoms + 36 * n_edges,
+        "k_embed_edge_bwd": T * n_atoms + 60 * n_edges,
+        "gemm_mix": 2 * T * n_atoms,
+        "k_rows_fill": 32 * n_atoms + 8 * n_cells + 24 * n_edges,
+        "k_rows_count": 32 * n_atoms + 8 * n_cells,
+    }
+    step = T * n_atoms * (14 * L + 8) + 52 * n_edges * (L + 1)          # SURVEY.md 8d, B_tn
+    nl = 48 * n_atoms + 8 * n_cells + 24 * n_edges                      # SURVEY.md 8d, B_nl
+    return per_kernel, step, nl
+
+
+def cpu_oracle_step(sample_atoms: int, full_nl: bool = True, seed: int = 11):
+    """Time the CPU oracle port: neighbor list (C, 1 core) on the full box + float64 TensorNet
+    (numpy, all BLAS threads) on a periodic sample of the same density; returns seconds per
+    full-size step (TensorNet part scaled by atom count) and a description."""
+    from paper_2402_17660_b200 import synth, init_params, TNConfig
+    from oracle import neighbors_oracle as O
+    from oracle import tensornet_oracle as T
+
+    t_nl = 0.0
+    n_full = 23558
+    if full_nl:
+        z, pos, batch, box = synth.config_c_box()
+        t0 = time.perf_counter()
+        O.build_neighbor_list(pos, batch, box, CUTOFF, 2 * 64 * n_full, strategy="cell",
+                              full_list=True, include_self_loops=True)
+        t_nl = time.perf_counter() - t0
+    edge = (sample_atoms / 0.09776) ** (1.0 / 3.0)
+    z, pos, batch, box = synth.config_c_box(n=sample_atoms, edge=edge, seed=seed)
+    cfg = TNConfig(embedding_dimension=CHANNELS, num_layers=LAYERS, num_rbf=NUM_RBF, cutoff_upper=CUTOFF)
+    params = init_params(cfg, 0)
+    ocfg = T.OracleConfig(CHANNELS, LAYERS, NUM_RBF, 0.0, CUTOFF)
+    t0 = time.perf_counter()
+    nl = O.build_neighbor_list(pos, batch, box, CUTOFF, 2 * 64 * sample_atoms, full_list=True,
+                               include_self_loops=True)
+    pr, dl, ds = nl.valid()
+    T.energy_forces_compact(params, ocfg, z, batch, pr, dl, ds)
+    t_tn = time.perf_counter() - t0
+    seconds = t_nl + t_tn * n_full / sample_atoms
+    return seconds, t_nl, t_tn
+
+
+def run_reference(args):
+    """Reference arm: the CPU implementation of the path (oracle port) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sample = 343
+    per_step = []
+    for it in range(args.warmup + args.steps):
+        sec, _, _ = cpu_oracle_step(sample, full_nl=True)
+        if it >= args.warmup:
+            per_step.append(sec)
+    ms = 1000.0 * float(np.mean(per_step))
+    value = 1000.0 / ms
+    desc = (f"per step: C-oracle cell neighbor list on the full 23,558-atom box (1 core) + float64 "
+            f"numpy TensorNet oracle (energy+forces) on a {sample}-atom periodic box of the same "
+            f"density, TensorNet time scaled by 23558/{sample}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C: 23,558-atom periodic cubic box (62.23 A), water-like species",
+                   "channels": CHANNELS, "layers": LAYERS, "num_rbf": NUM_RBF, "cutoff": CUTOFF},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def neighbor_sweep(torch, peak_gbs):
+    """Config B: neighbor-list us/call over particle counts (half list, like bench.py:133-138)."""
+    import paper_2402_17660_b200 as P
+    from paper_2402_17660_b200 import _lib, synth
+    from paper_2402_17660_b200.neighbors import NeighborEngine, plan_strategy
+
+    rows = []
+    for n in (1000, 4096, 16384, 65536, 262144, 1048576):
+        _, pos, batch, boxm = synth.config_b_cloud(n)
+        box = P.Box.from_matrix(boxm)
+        dev_pos = torch.from_numpy(pos).cuda()
+        dev_batch = torch.zeros(n, dtype=torch.int32, device="cuda")
+        for strategy in ("cell", "brute"):
+            if strategy == "brute" and n > 65536:
+                continue
+            code, dims, max_cells, _ = plan_strategy(n, box, CUTOFF, strategy)
+            cap = 32 * n
+            eng = NeighborEngine(n, 1, cap, box, 0.0, CUTOFF, code, dims, max_cells, 0)
+            eng.build(dev_pos, dev_batch)
+            torch.cuda.synchronize()
+            pairs = int(eng.counts[0].item())
+            reps = 20 if n <= 65536 else 5
+            if strategy == "brute" and n >= 65536:
+                reps = 2
+            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record()
+            for _ in range(reps):
+                eng.build(dev_pos, dev_batch)
+            stop.record()
+            torch.cuda.synchronize()
+            us = 1000.0 * start.elapsed_time(stop) / reps
+            ncell = int(eng.counts[2].item()) if strategy == "cell" else 0
+            nbytes = 48 * n + 8 * ncell + 40 * pairs      # float64 outputs: 8 + 24 + 8 B per row
+            rows.append({"n": n, "strategy": strategy, "us_per_call": round(us, 2), "pairs": pairs,
+                         "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peak_gbs, 4)})
+            del eng
+        del dev_pos, dev_batch
+        torch.cuda.empty_cache()
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C", choices=["A", "C", "D", "E"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2402_17660_b200 as P
+    from paper_2402_17660_b200 import _lib
+
+    peak_gbs, peak_src = load_peaks()
+    z, pos, batch, box, desc = workload(args.workload, rank, world)
+    n_atoms = len(pos)
+    n_samples = int(batch[-1]) + 1
+    model = P.TensorNet(embedding_dimension=CHANNELS, num_layers=LAYERS, num_rbf=NUM_RBF,
+                        cutoff_upper=CUTOFF, seed=0)
+    lib = _lib.load()
+
+    z_t = torch.from_numpy(np.array(z, dtype=np.int32))
+    pos_t = torch.from_numpy(np.array(pos, dtype=np.float32))
+    batch_t = None if n_samples == 1 else torch.from_numpy(np.array(batch, dtype=np.int32))
+    plan = model.prepare(z_t, pos_t, batch_t, box, n_samples=n_samples)
+    n_edges = int(plan.engine.counts[0].item())
+    n_cells = int(plan.engine.counts[2].item())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- launches per step + per-kernel device times (eager pass, CUDA events per kernel)
+    lib.nnp_launch_count(1)
+    model.enqueue_eager(plan)
+    torch.cuda.synchronize()
+    launches_per_step = lib.nnp_launch_count(1)
+    for _ in range(2):
+        model.enqueue_eager(plan)
+    torch.cuda.synchronize()
+    prof = {}
+    reps = 5
+    for _ in range(reps):
+        for k, (ms, cnt) in _lib.profile_step(lambda: model.enqueue_eager(plan)).items():
+            a = prof.setdefault(k, [0.0, 0])
+            a[0] += ms / reps
+            a[1] = cnt
+    kernel_ms = {k: round(v[0], 5) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    # ---- device-resident timing: K graph replays, CUDA events, max over ranks
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    for _ in range(args.warmup):
+        model.replay(plan)
+    barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(args.steps):
+        model.replay(plan)
+    stop.record()
+    barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    units = world if args.workload != "D" else 1        # replicas: every rank steps its own box
+    value = units * 1000.0 / ms_per_step
+
+    # ---- end to end through the public API with pinned host buffers
+    z_h, pos_h = z_t.pin_memory(), pos_t.pin_memory()
+    b_h = None if batch_t is None else batch_t.pin_memory()
+    e_h = torch.empty(n_samples, dtype=torch.float32).pin_memory()
+    f_h = torch.empty((n_atoms, 3), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        e, f = model.forward(z_h, pos_h, b_h, box, n_samples=n_samples, check=True, clone=False)
+        e_h.copy_(e, non_blocking=True)
+        f_h.copy_(f, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(3):
+        e2e_step()
+    barrier()
+    e2e_steps = max(10, args.steps // 2)
+    start.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    stop.record()
+    barrier()
+    e2e_ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = units * 1000.0 * e2e_steps / e2e_ms
+    if rank == 0:
+        # keep the GPU under the same load until nvidia-smi has at least a few samples
+        t_end = time.time() + 1.5
+        while len(sampler.lines) < 4 and time.time() < t_end:
+            model.replay(plan)
+            torch.cuda.synchronize()
+    clocks = sampler.stop() if rank == 0 else None
+    h2d = z_h.numel() * 4 + pos_h.numel() * 4 + (0 if b_h is None else b_h.numel() * 4)
+    d2h = e_h.numel() * 4 + f_h.numel() * 4 + 4      # + the overflow counter read
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel and of the whole step
+    per_kernel_bytes, step_bytes, nl_bytes = algorithmic_bytes(n_atoms, n_edges, n_cells)
+    dominant = next(iter(kernel_ms))
+    launches = prof[dominant][1]
+    roof = {"bound": "hbm", "kernel": dominant, "peak": peak_gbs, "unit": "GB/s", "peak_source": peak_src,
+            "achieved": None, "frac": None, "traffic": None, "launches_per_step": launches}
+    if dominant in per_kernel_bytes:
+        per_launch_ms = prof[dominant][0] / launches
+        achieved = per_kernel_bytes[dominant] / (per_launch_ms * 1e-3) / 1e9
+        roof.update({"achieved": round(achieved, 1), "frac": round(achieved / peak_gbs, 4),
+                     "algorithmic_bytes_per_launch": per_kernel_bytes[dominant],
+                     "avg_launch_ms": round(per_launch_ms, 5)})
+    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(traffic_path):
+        with open(traffic_path) as fh:
+            roof["traffic"] = json.load(fh).get(dominant)
+    step_roof = {"algorithmic_bytes": step_bytes + nl_bytes,
+                 "achieved_gbs": round((step_bytes + nl_bytes) / (ms_per_step * 1e-3) / 1e9, 1),
+                 "frac": round((step_bytes + nl_bytes) / (ms_per_step * 1e-3) / 1e9 / peak_gbs, 4)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak" if args.workload != "D" else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "atoms": n_atoms, "samples": n_samples, "directed_edges": n_edges,
+                   "channels": CHANNELS, "layers": LAYERS, "num_rbf": NUM_RBF, "cutoff": CUTOFF,
+                   "parallelism": "replicas only" if args.workload != "D" else f"molecules/{world}",
+                   "l2_note": "working set per step (saved activations ~1.3 GB) exceeds the 126 MB L2; no flush",
+                   "msteps_per_day": round(86.4 / ms_per_step, 3)},
+        "clocks": clocks,
+        "e2e": {"value": round(e2e_value, 3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / e2e_steps, 4)},
+        "gpu_launches": launches_per_step * args.steps,
+        "launches_per_step": launches_per_step,
+        "roofline": roof,
+        "step_roofline": step_roof,
+        "kernel_ms": kernel_ms,
+    }
+    if world == 1 and not args.no_cpu and args.workload == "C":
+        sec, t_nl, t_tn = cpu_oracle_step(1000)
+        line["cpu_baseline"] = {
+            "value": round(1.0 / sec, 5), "unit": "steps/s", "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": (f"C-oracle cell neighbor list on the full 23,558-atom box ({t_nl:.2f} s, 1 core) + "
+                       f"float64 numpy TensorNet oracle energy+forces on a 1000-atom periodic box of the "
+                       f"same density ({t_tn:.1f} s, BLAS threads = all cores), scaled by 23558/1000"),
+        }
+    if world == 1 and not args.no_sweep:
+        line["neighbor_sweep"] = neighbor_sweep(torch, peak_gbs)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -171,6 +171,14 @@ int nnp_test_gemm_nt(const float *A, const float *W, const float *bias, float *o
 /* Test hook: 1 = 3xTF32 tensor-core inner loop (default), 0 = FP32 FFMA inner loop. */
 int nnp_set_gemm_mode(int use_mma);
 
+/* Instrumentation (bench.py / tests): number of kernels this library has enqueued so far
+ * (reset != 0 clears it), and per-kernel device times measured with CUDA events on the
+ * launching stream: nnp_profile_begin() arms it, nnp_profile_report() synchronises and writes
+ * "label total_ms launches\n" lines. */
+int nnp_launch_count(int reset);
+int nnp_profile_begin(void);
+int nnp_profile_report(char *buf, int buf_bytes);
+
 #ifdef __cplusplus
 }
 #endif

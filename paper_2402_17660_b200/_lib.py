@@ -26,7 +26,8 @@ TN_MAX_LAYERS = 8
 EXPORTED_SYMBOLS = (
     "nnp_last_error", "nnp_version", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
     "nnp_distance_pullback", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
-    "nnp_test_gemm_nt", "nnp_set_gemm_mode",
+    "nnp_test_gemm_nt", "nnp_set_gemm_mode", "nnp_launch_count", "nnp_profile_begin",
+    "nnp_profile_report",
 )
 
 _f = ctypes.c_float
@@ -94,6 +95,9 @@ def load() -> ctypes.CDLL:
     ]
     lib.nnp_test_gemm_nt.argtypes = [_p, _p, _p, _p, _i32, _i32, _i32, _p]
     lib.nnp_set_gemm_mode.argtypes = [ctypes.c_int]
+    lib.nnp_launch_count.argtypes = [ctypes.c_int]
+    lib.nnp_profile_begin.argtypes = []
+    lib.nnp_profile_report.argtypes = [ctypes.c_char_p, ctypes.c_int]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(lib, name)
         if name not in ("nnp_last_error",):
@@ -131,3 +135,18 @@ def current_stream() -> int:
     import torch
 
     return torch.cuda.current_stream().cuda_stream
+
+
+def profile_step(fn):
+    """Run ``fn()`` (which enqueues kernels eagerly) with per-kernel CUDA-event timing.
+    Returns {label: (total_ms, launches)} in launch order."""
+    lib = load()
+    lib.nnp_profile_begin()
+    fn()
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.nnp_profile_report(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, ms, cnt = line.split()
+        out[name] = (float(ms), int(cnt))
+    return out

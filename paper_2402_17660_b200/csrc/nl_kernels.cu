@@ -592,48 +592,54 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
     const int n = a.n;
     const int nb = nnp_blocks(n, 256);
     cudaMemsetAsync(counts, 0, 4 * sizeof(int), stream);
-    k_fill_i32<<<nnp_blocks(a.n_samples + 1, 256), 256, 0, stream>>>(a.sample_ptr, a.n_samples + 1, n);
-    k_sample_ptr<<<nb, 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr);
+    { NNP_PROF("k_fill_i32", stream); k_fill_i32<<<NNP_GRID(nnp_blocks(a.n_samples + 1, 256)), 256, 0, stream>>>(a.sample_ptr, a.n_samples + 1, n); }
+    { NNP_PROF("k_sample_ptr", stream); k_sample_ptr<<<NNP_GRID(nb), 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr); }
 
     if (a.strategy == NNP_STRATEGY_CELL) {
         int n_partial = 1;
         if (!a.periodic) {
             n_partial = std::min(BOUNDS_BLOCKS, nb);
-            k_bounds_partial<<<n_partial, NL_THREADS, 0, stream>>>(pos, n, a.bounds_partial);
+            { NNP_PROF("k_bounds_partial", stream); k_bounds_partial<<<NNP_GRID(n_partial), NL_THREADS, 0, stream>>>(pos, n, a.bounds_partial); }
         }
-        k_grid_setup<<<1, 32, 0, stream>>>(a, n_partial);
+        { NNP_PROF("k_grid_setup", stream); k_grid_setup<<<NNP_GRID(1), 32, 0, stream>>>(a, n_partial); }
         cudaMemsetAsync(a.cell_start, 0, ((size_t)a.max_cells + 1) * sizeof(int), stream);
         cudaMemsetAsync(a.cell_cursor, 0, (size_t)a.max_cells * sizeof(int), stream);
-        k_cell_assign<<<nb, 256, 0, stream>>>(a);
-        rc = nnp_exclusive_scan_i32(a.cell_start, a.cell_start, (int64_t)a.max_cells + 1, scan_temp,
-                                    stream);
+        { NNP_PROF("k_cell_assign", stream); k_cell_assign<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
+        {
+            NNP_PROF("scan_cells", stream);
+            rc = nnp_exclusive_scan_i32(a.cell_start, a.cell_start, (int64_t)a.max_cells + 1,
+                                        scan_temp, stream);
+        }
         if (rc) return rc;
-        k_cell_scatter<<<nb, 256, 0, stream>>>(a);
-        k_cell_rank<<<nb, 256, 0, stream>>>(a);
+        { NNP_PROF("k_cell_scatter", stream); k_cell_scatter<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
+        { NNP_PROF("k_cell_rank", stream); k_cell_rank<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
     } else {
-        k_identity_order<<<nb, 256, 0, stream>>>(a);
+        { NNP_PROF("k_identity_order", stream); k_identity_order<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
     }
     NNP_CHECK_LAUNCH("neighbor binning");
 
     const int row_blocks = nnp_blocks(n, NL_WARPS);
     const bool f32 = p->flags & NNP_NL_F32_OUT;
-    k_rows<false, double><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+    { NNP_PROF("k_rows_count", stream); k_rows<false, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
     // row_count has n entries; entry n must be zero so the scan's last output is the total
     cudaMemsetAsync(a.row_count + n, 0, sizeof(int), stream);
-    rc = nnp_exclusive_scan_i32(a.row_count, a.row_ptr, (int64_t)n + 1, scan_temp, stream);
+    {
+        NNP_PROF("scan_rows", stream);
+        rc = nnp_exclusive_scan_i32(a.row_count, a.row_ptr, (int64_t)n + 1, scan_temp, stream);
+    }
     if (rc) return rc;
-    k_total<<<1, 32, 0, stream>>>(a);
+    { NNP_PROF("k_total", stream); k_total<<<NNP_GRID(1), 32, 0, stream>>>(a); }
     if (f32)
-        k_rows<true, float><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+        { NNP_PROF("k_rows_fill", stream); k_rows<true, float><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
     else
-        k_rows<true, double><<<row_blocks, NL_THREADS, 0, stream>>>(a);
+        { NNP_PROF("k_rows_fill", stream); k_rows<true, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
     if (!(p->flags & NNP_NL_NO_PAD)) {
         if (f32)
-            k_pad_tail<float><<<nnp_blocks(a.capacity, 256), 256, 0, stream>>>(a);
+            { NNP_PROF("k_pad_tail", stream); k_pad_tail<float><<<NNP_GRID(nnp_blocks(a.capacity, 256)), 256, 0, stream>>>(a); }
         else
-            k_pad_tail<double><<<nnp_blocks(a.capacity, 256), 256, 0, stream>>>(a);
+            { NNP_PROF("k_pad_tail", stream); k_pad_tail<double><<<NNP_GRID(nnp_blocks(a.capacity, 256)), 256, 0, stream>>>(a); }
     }
-    if (order) k_copy_order<<<nb, 256, 0, stream>>>(a);
+    if (order) k_copy_order<<<NNP_GRID(nb), 256, 0, stream>>>(a);
     NNP_CHECK_LAUNCH("neighbor rows");
     return NNP_OK;
 }
@@ -642,7 +648,7 @@ extern "C" int nnp_f32_to_f64(const float *src, double *dst, int64_t n, nnp_stre
 {
     NNP_CHECK_ARG(src && dst && n >= 0, "bad arguments to nnp_f32_to_f64");
     if (n == 0) return NNP_OK;
-    k_f32_to_f64<<<nnp_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+    k_f32_to_f64<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
     NNP_CHECK_LAUNCH("f32_to_f64");
     return NNP_OK;
 }
@@ -652,13 +658,15 @@ extern "C" int nnp_distance_pullback(const int32_t *pairs, const double *deltas,
                                      int32_t n_atoms, double *grad, int32_t *flag_out,
                                      nnp_stream_t stream_)
 {
-    NNP_CHECK_ARG(pairs && deltas && dists && g && grad && flag_out && count >= 0 && n_atoms >= 1,
+    NNP_CHECK_ARG(grad && flag_out && count >= 0 && n_atoms >= 1,
                   "bad arguments to nnp_distance_pullback");
+    NNP_CHECK_ARG(count == 0 || (pairs && deltas && dists && g),
+                  "NULL edge buffer passed to nnp_distance_pullback");
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     cudaMemsetAsync(grad, 0, 3 * (size_t)n_atoms * sizeof(double), stream);
     cudaMemsetAsync(flag_out, 0x7f, sizeof(int), stream);  // 0x7f7f7f7f = none
     if (count > 0)
-        k_pullback<<<nnp_blocks(count, 256), 256, 0, stream>>>(pairs, deltas, dists, g, count, grad,
+        k_pullback<<<NNP_GRID(nnp_blocks(count, 256)), 256, 0, stream>>>(pairs, deltas, dists, g, count, grad,
                                                               flag_out);
     NNP_CHECK_LAUNCH("distance_pullback");
     return NNP_OK;

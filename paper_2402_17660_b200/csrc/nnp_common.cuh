@@ -29,6 +29,22 @@ void nnp_set_error(const char *fmt, ...);
         }                                                                       \
     } while (0)
 
+// ---- launch accounting and per-kernel timing (test/bench instrumentation)
+extern int g_nnp_launch_count;
+// wraps the grid argument of every launch: counts kernels enqueued by this library
+#define NNP_GRID(x) (++g_nnp_launch_count, (x))
+
+// When profiling is on (nnp_profile_begin), NNP_PROF scopes record a cudaEvent pair around the
+// launches they enclose; nnp_profile_report sums the elapsed time per label.
+void nnp_prof_mark(const char *label, cudaStream_t stream, int begin);
+struct NnpProfScope {
+    const char *label;
+    cudaStream_t stream;
+    NnpProfScope(const char *l, cudaStream_t s) : label(l), stream(s) { nnp_prof_mark(l, s, 1); }
+    ~NnpProfScope() { nnp_prof_mark(label, stream, 0); }
+};
+#define NNP_PROF(label, stream) NnpProfScope nnp_prof_scope_##__LINE__(label, stream)
+
 static inline size_t nnp_align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller-provided workspace; with base == nullptr it only measures.

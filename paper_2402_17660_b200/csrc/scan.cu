@@ -15,6 +15,80 @@ void nnp_set_error(const char *fmt, ...)
 }
 
 extern "C" const char *nnp_last_error(void) { return g_last_error; }
+
+int g_nnp_launch_count = 0;
+extern "C" int nnp_launch_count(int reset)
+{
+    int v = g_nnp_launch_count;
+    if (reset) g_nnp_launch_count = 0;
+    return v;
+}
+
+// ---- per-kernel timing with CUDA events on the launching stream
+#include <map>
+#include <string>
+#include <vector>
+namespace {
+struct ProfRec {
+    const char *label;
+    cudaEvent_t start, stop;
+};
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_recs;
+}  // namespace
+
+void nnp_prof_mark(const char *label, cudaStream_t stream, int begin)
+{
+    if (!g_prof_on) return;
+    if (begin) {
+        ProfRec r{label, nullptr, nullptr};
+        cudaEventCreate(&r.start);
+        cudaEventCreate(&r.stop);
+        cudaEventRecord(r.start, stream);
+        g_prof_recs.push_back(r);
+    } else {
+        for (size_t i = g_prof_recs.size(); i-- > 0;)
+            if (g_prof_recs[i].label == label) {
+                cudaEventRecord(g_prof_recs[i].stop, stream);
+                break;
+            }
+    }
+}
+
+extern "C" int nnp_profile_begin(void)
+{
+    g_prof_on = true;
+    return NNP_OK;
+}
+
+// Synchronises, writes "label total_ms count\n" lines into buf, clears the records.
+extern "C" int nnp_profile_report(char *buf, int buf_bytes)
+{
+    g_prof_on = false;
+    cudaDeviceSynchronize();
+    std::map<std::string, std::pair<double, int>> acc;
+    std::vector<std::string> order;
+    for (auto &r : g_prof_recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.start, r.stop);
+        if (!acc.count(r.label)) order.push_back(r.label);
+        acc[r.label].first += ms;
+        acc[r.label].second += 1;
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    g_prof_recs.clear();
+    std::string out;
+    for (auto &k : order) {
+        char line[160];
+        snprintf(line, sizeof(line), "%s %.6f %d\n", k.c_str(), acc[k].first, acc[k].second);
+        out += line;
+    }
+    if (buf && buf_bytes > 0) {
+        snprintf(buf, (size_t)buf_bytes, "%s", out.c_str());
+    }
+    return NNP_OK;
+}
 extern "C" int nnp_version(void) { return 100; }
 
 namespace {
@@ -110,10 +184,10 @@ int nnp_exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, int32_t *
 {
     if (n <= 0) return NNP_OK;
     const int nt = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
-    scan_tiles<<<nt, SCAN_THREADS, 0, stream>>>(in, out, n, temp);
+    scan_tiles<<<NNP_GRID(nt), SCAN_THREADS, 0, stream>>>(in, out, n, temp);
     if (nt > 1) {
-        scan_totals<<<1, SCAN_THREADS, 0, stream>>>(temp, nt);
-        scan_add<<<nt, SCAN_THREADS, 0, stream>>>(out, n, temp);
+        scan_totals<<<NNP_GRID(1), SCAN_THREADS, 0, stream>>>(temp, nt);
+        scan_add<<<NNP_GRID(nt), SCAN_THREADS, 0, stream>>>(out, n, temp);
     }
     NNP_CHECK_LAUNCH("exclusive_scan");
     return NNP_OK;

@@ -220,9 +220,9 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
     if (maxM <= 0) return NNP_OK;
     dim3 grid((maxM + GEMM_BM - 1) / GEMM_BM, (maxN + GEMM_BN - 1) / GEMM_BN, count);
     if (g_nnp_gemm_use_mma)
-        gemm_nt_kernel<PRO, EPI, true><<<grid, GEMM_THREADS, 0, stream>>>(b);
+        gemm_nt_kernel<PRO, EPI, true><<<NNP_GRID(grid), GEMM_THREADS, 0, stream>>>(b);
     else
-        gemm_nt_kernel<PRO, EPI, false><<<grid, GEMM_THREADS, 0, stream>>>(b);
+        gemm_nt_kernel<PRO, EPI, false><<<NNP_GRID(grid), GEMM_THREADS, 0, stream>>>(b);
     NNP_CHECK_LAUNCH("gemm_nt");
     return NNP_OK;
 }

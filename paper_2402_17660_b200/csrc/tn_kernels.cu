@@ -882,93 +882,93 @@ int run_step(TnDev &d, cudaStream_t st)
         if (rc) return rc; \
     } while (0)
 
-    k_fill_int<<<nnp_blocks(d.n_samples + 1, 256), 256, 0, st>>>(d.sample_ptr, d.n_samples + 1, n);
-    k_prep_nodes<<<nnp_blocks(n, 256), 256, 0, st>>>(d);
-    k_edge_geom<<<nnp_blocks(d.capacity, 256), 256, 0, st>>>(d);
+    { NNP_PROF("k_fill_int", st); k_fill_int<<<NNP_GRID(nnp_blocks(d.n_samples + 1, 256)), 256, 0, st>>>(d.sample_ptr, d.n_samples + 1, n); }
+    { NNP_PROF("k_prep_nodes", st); k_prep_nodes<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d); }
+    { NNP_PROF("k_edge_geom", st); k_edge_geom<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
 
     // ---- embedding
-    k_embed_edge<C><<<warp_blocks, 256, 0, st>>>(d);
+    { NNP_PROF("k_embed_edge", st); k_embed_edge<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.ln0, m.es0_w, m.es0_b, d.e0, n, 2 * C, C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
         b.g[0] = plain_gemm(d.e0, m.es1_w, m.es1_b, d.e1, n, 3 * C, 2 * C);
-        RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
         GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xa, n, C, d.Xm, d.e1, 3 * C);
-        RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st)));
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st))); }
     }
     float *X = d.Xa, *Xother = d.Xb;
 
     // ---- interaction layers
     for (int l = 0; l < L; ++l) {
-        k_normalize<<<ew_blocks, 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C);
+        { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st)));
-        k_edge_message<C><<<warp_blocks, 256, 0, st>>>(d, l);
-        k_node_product<<<ew_blocks, 256, 0, st>>>(d.Mc[l], d.Yc[l], d.Qc, n, C);
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
+        { NNP_PROF("k_edge_message", st); k_edge_message<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, l); }
+        { NNP_PROF("k_node_product", st); k_node_product<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], d.Qc, n, C); }
         GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + (size_t)3 * C * C, d.Dc[l], n, C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st)));
-        k_residual<<<ew_blocks, 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, n, C);
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
+        { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, n, C); }
         std::swap(X, Xother);
     }
 
     // ---- readout
-    k_readout_feats<C><<<warp_blocks, 256, 0, st>>>(d, X);
+    { NNP_PROF("k_readout_feats", st); k_readout_feats<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, X); }
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.lnr, m.lin_w, m.lin_b, d.r0, n, C, 3 * C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
         b.g[0] = plain_gemm(d.r0, m.h1_w, m.h1_b, d.r1, n, H, C);
-        RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
     }
-    k_head<<<warp_blocks, 256, 0, st>>>(d, H);
-    k_energy_sum<<<d.n_samples, 256, 0, st>>>(d);
-    if (d.per_atom) k_copy_per_atom<<<nnp_blocks(n, 256), 256, 0, st>>>(d);
+    { NNP_PROF("k_head", st); k_head<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, H); }
+    { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), 256, 0, st>>>(d); }
+    if (d.per_atom) k_copy_per_atom<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d);
     NNP_CHECK_LAUNCH("tensornet forward");
     if (!d.forces) return NNP_OK;
 
     // ================================================================= reverse sweep
-    k_head_bwd<<<nnp_blocks((int64_t)n * H, 256), 256, 0, st>>>(d, H);
+    { NNP_PROF("k_head_bwd", st); k_head_bwd<<<NNP_GRID(nnp_blocks((int64_t)n * H, 256)), 256, 0, st>>>(d, H); }
     {
         GemmBatch b{};
         // g_r0 = (g_r1 @ h1_w) * silu'(r0)
         b.g[0] = plain_gemm(d.g_r1, m.h1_wT, nullptr, d.g_r0, n, C, H, d.r0, C);
-        RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st))); }
         b.g[0] = plain_gemm(d.g_r0, m.lin_wT, nullptr, d.g_lnr, n, 3 * C, C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
     }
     float *GX = d.G1, *Ga = d.G2, *Gb = d.G3;
-    k_readout_bwd<C><<<warp_blocks, 256, 0, st>>>(d, X, GX);
+    { NNP_PROF("k_readout_bwd", st); k_readout_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, X, GX); }
 
     for (int l = L - 1; l >= 0; --l) {
         // GX = dL/dX_{l+1}.  dL/dXh starts as GX itself.
-        k_residual_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Dc[l], Ga, n, C);              // Ga = G_D
+        { NNP_PROF("k_residual_bwd", st); k_residual_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Dc[l], Ga, n, C); }  // Ga = G_D
         GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + (size_t)3 * C * C, Gb, n, C);     // Gb = G_Q
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st)));
-        k_node_product_bwd<<<ew_blocks, 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C);
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
+        { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        k_edge_message_bwd<C><<<warp_blocks, 256, 0, st>>>(d, l, Ga, d.Qc);
+        { NNP_PROF("k_edge_message_bwd", st); k_edge_message_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, l, Ga, d.Qc); }
         // G_Xh = GX + mix^T(G_Y)  -> written in place over GX
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GX, n, C, nullptr, GX, C);
-        RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st)));
-        k_normalize_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Xh[l], d.nx[l], Gb, n, C);
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st))); }
+        { NNP_PROF("k_normalize_bwd", st); k_normalize_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Xh[l], d.nx[l], Gb, n, C); }
         std::swap(GX, Gb);
     }
 
     // ---- embedding reverse: X = Xm * gate
-    k_embed_gate_bwd<<<ew_blocks, 256, 0, st>>>(GX, d.Xm, d.e1, Ga, d.g_e1, n, C);     // Ga = G_Xm
+    { NNP_PROF("k_embed_gate_bwd", st); k_embed_gate_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Xm, d.e1, Ga, d.g_e1, n, C); }  // Ga = G_Xm
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.g_e1, m.es1_wT, nullptr, d.g_e0, n, 2 * C, 3 * C, d.e0, 2 * C);
-        RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st))); }
         b.g[0] = plain_gemm(d.g_e0, m.es0_wT, nullptr, d.g_ln0, n, C, 2 * C);
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st)));
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
         GemmBatch mx = mix_gemm(Ga, m.et_wT, Gb, n, C);                                 // Gb = G_X0 part
-        RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st)));
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
-    k_embed_norm_bwd<C><<<warp_blocks, 256, 0, st>>>(d, Gb);
-    k_embed_edge_bwd<C><<<warp_blocks, 256, 0, st>>>(d, Gb);
-    k_forces<<<nnp_blocks(n, 128), 128, 0, st>>>(d);
+    { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
+    { NNP_PROF("k_embed_edge_bwd", st); k_embed_edge_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
+    { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(nnp_blocks(n, 128)), 128, 0, st>>>(d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
     return NNP_OK;

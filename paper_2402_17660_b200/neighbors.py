@@ -215,8 +215,8 @@ def build_neighbor_list(system: System, spec: NeighborSpec) -> NeighborList:
         _lib.NL_SELF_LOOPS if spec.include_self_loops else 0)
     eng = NeighborEngine(n, system.n_samples, spec.capacity, box, spec.cutoff_lower,
                          spec.cutoff_upper, code, dims, max_cells, flags)
-    pos = torch.as_tensor(np.ascontiguousarray(system.positions, dtype=np.float64)).to(eng.device)
-    batch = torch.as_tensor(np.ascontiguousarray(system.batch, dtype=np.int32)).to(eng.device)
+    pos = torch.from_numpy(np.array(system.positions, dtype=np.float64, order="C")).to(eng.device)
+    batch = torch.from_numpy(np.array(system.batch, dtype=np.int32, order="C")).to(eng.device)
     eng.build(pos, batch)
     counts = eng.counts.cpu().numpy()          # synchronises the stream
     total = int(counts[0])
