@@ -102,6 +102,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         if name not in ("nnp_last_error",):
             fn.restype = ctypes.c_int
+    if "NNP_GEMM_MODE" in os.environ:       # 2 = tcgen05, 1 = mma.sync, 0 = FFMA (measurements)
+        lib.nnp_set_gemm_mode(int(os.environ["NNP_GEMM_MODE"]))
     _lib = lib
     return lib
 

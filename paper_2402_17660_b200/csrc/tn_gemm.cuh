@@ -78,6 +78,48 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs &g, int r, int c, f
     }
 }
 
+// four consecutive columns c..c+3 of one row (c % 4 == 0; all leading dimensions % 4 == 0)
+template <int EPI>
+__device__ __forceinline__ void gemm_epilogue4(const GemmArgs &g, int r, int c, float4 v)
+{
+    if (r >= g.M || c >= g.N) return;
+    const int pr = gemm_phys_row(g, r);
+    if (g.bias) {
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(g.bias + c));
+        v.x += b.x;
+        v.y += b.y;
+        v.z += b.z;
+        v.w += b.w;
+    }
+    const size_t o = (size_t)pr * g.ldo + c;
+    if (EPI == EPI_STORE) {
+        *reinterpret_cast<float4 *>(g.out + o) = v;
+    } else if (EPI == EPI_MUL_SILU_GRAD) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(g.aux + (size_t)pr * g.ldaux + c));
+        v.x *= nnp_silu_grad(a.x);
+        v.y *= nnp_silu_grad(a.y);
+        v.z *= nnp_silu_grad(a.z);
+        v.w *= nnp_silu_grad(a.w);
+        *reinterpret_cast<float4 *>(g.out + o) = v;
+    } else if (EPI == EPI_GATE) {
+        const int node = g.ncomp ? r / g.ncomp : r;
+        const float *a = g.aux + (size_t)node * g.ldaux + 3 * c + g.grp;
+        *reinterpret_cast<float4 *>(g.out2 + o) = v;
+        v.x *= nnp_silu(__ldg(a));
+        v.y *= nnp_silu(__ldg(a + 3));
+        v.z *= nnp_silu(__ldg(a + 6));
+        v.w *= nnp_silu(__ldg(a + 9));
+        *reinterpret_cast<float4 *>(g.out + o) = v;
+    } else {
+        const float4 a = *reinterpret_cast<const float4 *>(g.aux + (size_t)pr * g.ldaux + c);
+        v.x += a.x;
+        v.y += a.y;
+        v.z += a.z;
+        v.w += a.w;
+        *reinterpret_cast<float4 *>(g.out + o) = v;
+    }
+}
+
 template <int PRO, int EPI, bool MMA>
 __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
 {
@@ -203,26 +245,4 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
     }
 }
 
-extern int g_nnp_gemm_use_mma;  // 1 = 3xTF32 tensor cores (default), 0 = FP32 FFMA
-
-template <int PRO, int EPI>
-static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
-{
-    int maxM = 0, maxN = 0;
-    for (int i = 0; i < count; ++i) {
-        maxM = b.g[i].M > maxM ? b.g[i].M : maxM;
-        maxN = b.g[i].N > maxN ? b.g[i].N : maxN;
-        if (b.g[i].K % 4 != 0 || b.g[i].lda % 4 != 0) {
-            nnp_set_error("gemm: K=%d and lda=%d must be multiples of 4", b.g[i].K, b.g[i].lda);
-            return NNP_ERR_INVALID;
-        }
-    }
-    if (maxM <= 0) return NNP_OK;
-    dim3 grid((maxM + GEMM_BM - 1) / GEMM_BM, (maxN + GEMM_BN - 1) / GEMM_BN, count);
-    if (g_nnp_gemm_use_mma)
-        gemm_nt_kernel<PRO, EPI, true><<<NNP_GRID(grid), GEMM_THREADS, 0, stream>>>(b);
-    else
-        gemm_nt_kernel<PRO, EPI, false><<<NNP_GRID(grid), GEMM_THREADS, 0, stream>>>(b);
-    NNP_CHECK_LAUNCH("gemm_nt");
-    return NNP_OK;
-}
+extern int g_nnp_gemm_use_mma;  // 2 = tcgen05 3xTF32 (default), 1 = mma.sync 3xTF32, 0 = FP32 FFMA

@@ -1,0 +1,338 @@
+// tcgen05 (5th-generation tensor core) inner loop for the node-level channel-mixing GEMMs.
+//
+//   out[r, n] = sum_k A[r, k] * W[n, k]      rows r possibly addressed through [node][9][C]
+//
+// One CTA owns a 128-row x NT-column output tile whose FP32 accumulator lives in TMEM
+// (128 lanes x NT columns).  The FP32 operands are split on the fly into TF32 pairs
+// (x = x_hi + x_lo) and each 8-wide K step issues three tcgen05.mma.kind::tf32:
+//     D += A_lo*W_hi ;  D += A_hi*W_lo ;  D += A_hi*W_hi         ("3xTF32": FP32-level accuracy)
+// Operands are staged in shared memory in the canonical K-major SWIZZLE_128B layout (8-row x
+// 128-byte atoms, 16-byte chunks XOR-swizzled by the row index); one K chunk = 32 floats = one
+// swizzle row.  Because the split needs registers, the producer is the whole CTA (coalesced
+// float4 loads -> cvt.rna.tf32 -> st.shared), made visible to the tensor core's async proxy with
+// fence.proxy.async; a single elected thread issues the MMAs and commits them to an mbarrier that
+// gates the reuse of the staging buffer.  The next chunk's global loads are issued before that
+// wait, so they overlap the MMAs; several CTAs per SM (<= 65 KB shared memory, <= 128 TMEM
+// columns each) overlap each other's epilogues.  The epilogue reads the accumulator back with
+// tcgen05.ld (32 lanes x 32 bit, 16 columns at a time): thread t of warp w owns output row
+// 32*w + t.
+#pragma once
+
+#include <algorithm>
+
+#include "tn_gemm.cuh"
+
+namespace tc5 {
+
+constexpr int BM = 128;      // UMMA M
+constexpr int KC = 32;       // floats per K chunk = one 128-byte swizzle row
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    for (long spin = 0; !done; ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (spin > (1L << 28)) __trap();  // never hang the device on a protocol error
+    }
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (cute::UMMA::SmemDescriptor layout):
+// start address >> 4 in [0,14), LBO >> 4 in [16,30) (unused for swizzled K-major: 1),
+// SBO >> 4 in [32,46) = 1024 B between 8-row atoms, version 1 in [46,48), layout type 2 in [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr)
+{
+    uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// kind::tf32 instruction descriptor: D = F32 (bit 4), A = B = TF32 (2 at bits 7 and 10),
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+__device__ __forceinline__ uint32_t make_idesc(int n)
+{
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of the 16-byte chunk (row r, chunk j of 8) inside a [rows][128 B] swizzled tile
+__device__ __forceinline__ uint32_t swz(int r, int j)
+{
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ void split_store(char *hi_base, char *lo_base, uint32_t off, float4 v)
+{
+    uint32_t h[4], l[4];
+    tf32_split(v.x, h[0], l[0]);
+    tf32_split(v.y, h[1], l[1]);
+    tf32_split(v.z, h[2], l[2]);
+    tf32_split(v.w, h[3], l[3]);
+    *reinterpret_cast<uint4 *>(hi_base + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4 *>(lo_base + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// NT: output columns per CTA (16..128, multiple of 16); TMEM_COLS: power of two >= max(NT, 32)
+template <int PRO, int EPI, int NT>
+__global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
+{
+    constexpr int TMEM_COLS = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
+    constexpr int A_PASSES = BM / 16;   // 128 threads cover 16 rows x 8 chunks per pass
+    constexpr int W_PASSES = NT / 16;
+    const GemmArgs g = batch.g[blockIdx.z];
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * NT;
+    if (m0 >= g.M || n0 >= g.N) return;
+
+    extern __shared__ char smem_raw[];
+    char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    char *a_hi = smem, *a_lo = smem + BM * 128;
+    char *w_hi = smem + 2 * BM * 128, *w_lo = w_hi + NT * 128;
+    __shared__ uint64_t mma_bar;
+    __shared__ uint32_t tmem_base_s;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&mma_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "n"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_d = tmem_base_s;
+
+    // loader mapping: 8 threads per row (one 16-byte chunk each), 16 rows per pass
+    const int lrow = tid >> 3, lchunk = tid & 7;
+    const float *a_ptr[A_PASSES];
+#pragma unroll
+    for (int p = 0; p < A_PASSES; ++p) {
+        const int r = m0 + p * 16 + lrow;
+        a_ptr[p] = r < g.M ? g.A + (size_t)gemm_phys_row(g, r) * g.lda + lchunk * 4 : nullptr;
+    }
+    const float *w_ptr[W_PASSES];
+#pragma unroll
+    for (int p = 0; p < W_PASSES; ++p) {
+        const int n = n0 + p * 16 + lrow;
+        w_ptr[p] = n < g.N ? g.W + (size_t)n * g.K + lchunk * 4 : nullptr;
+    }
+
+    const int nchunks = (g.K + KC - 1) / KC;
+    float4 ra[A_PASSES], rw[W_PASSES];
+    auto load_chunk = [&](int c) {
+        const int k0 = c * KC;
+        const bool k_ok = k0 + lchunk * 4 < g.K;
+#pragma unroll
+        for (int p = 0; p < A_PASSES; ++p) {
+            ra[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a_ptr[p] && k_ok) ra[p] = __ldg(reinterpret_cast<const float4 *>(a_ptr[p] + k0));
+        }
+#pragma unroll
+        for (int p = 0; p < W_PASSES; ++p) {
+            rw[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (w_ptr[p] && k_ok) rw[p] = __ldg(reinterpret_cast<const float4 *>(w_ptr[p] + k0));
+        }
+    };
+
+    const uint32_t idesc = make_idesc(NT);
+    const uint64_t da_hi = make_desc(smem_u32(a_hi)), da_lo = make_desc(smem_u32(a_lo));
+    const uint64_t dw_hi = make_desc(smem_u32(w_hi)), dw_lo = make_desc(smem_u32(w_lo));
+
+    load_chunk(0);
+    for (int c = 0; c < nchunks; ++c) {
+        if (c > 0) {
+            mbar_wait(&mma_bar, (uint32_t)((c - 1) & 1));   // MMAs of chunk c-1 have read the buffers
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+#pragma unroll
+        for (int p = 0; p < A_PASSES; ++p) {
+            float4 v = ra[p];
+            if (PRO == PRO_SILU) {
+                v.x = nnp_silu(v.x);
+                v.y = nnp_silu(v.y);
+                v.z = nnp_silu(v.z);
+                v.w = nnp_silu(v.w);
+            }
+            split_store(a_hi, a_lo, swz(p * 16 + lrow, lchunk), v);
+        }
+#pragma unroll
+        for (int p = 0; p < W_PASSES; ++p) split_store(w_hi, w_lo, swz(p * 16 + lrow, lchunk), rw[p]);
+        // generic-proxy writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+                const uint64_t adv = (uint64_t)(ks * 32 >> 4);   // 8 tf32 = 32 bytes along K
+                umma_tf32(tmem_d, da_lo + adv, dw_hi + adv, idesc, (c | ks) != 0);
+                umma_tf32(tmem_d, da_hi + adv, dw_lo + adv, idesc, 1);
+                umma_tf32(tmem_d, da_hi + adv, dw_hi + adv, idesc, 1);
+            }
+            umma_commit(&mma_bar);
+        }
+        if (c + 1 < nchunks) load_chunk(c + 1);             // overlaps the MMAs just issued
+    }
+    mbar_wait(&mma_bar, (uint32_t)((nchunks - 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // epilogue, phase 1: TMEM -> registers -> shared memory.  Thread (warp, lane) owns accumulator
+    // lane 32*warp + lane = one output row; the operand buffers are free now and are reused as a
+    // [128][NT] staging tile whose 16-byte chunks are XOR-swizzled by the row so that both the
+    // row-per-thread writes here and the row-per-warp reads below are conflict-free.
+    constexpr int CH = NT / 4;
+    float *stage = reinterpret_cast<float *>(smem);
+    {
+        const int rr = warp * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int pos = ((c0 >> 2) + q) ^ (rr & (CH - 1));
+                *reinterpret_cast<float4 *>(stage + rr * NT + pos * 4) =
+                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+        }
+    }
+    __syncthreads();
+    // phase 2: one warp per row, one float4 per lane -> coalesced global stores
+    constexpr int ROWS_PER_IT = 32 / CH;          // rows a warp covers per iteration (NT < 128)
+    for (int it = warp * ROWS_PER_IT; it < BM; it += 4 * ROWS_PER_IT) {
+        const int rr = it + lane / CH;
+        const int ch = lane % CH;
+        const int pos = ch ^ (rr & (CH - 1));
+        const float4 v = *reinterpret_cast<const float4 *>(stage + rr * NT + pos * 4);
+        gemm_epilogue4<EPI>(g, m0 + rr, n0 + ch * 4, v);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+template <int PRO, int EPI, int NT>
+static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStream_t stream)
+{
+    const int smem = 2 * BM * 128 + 2 * NT * 128 + 1024;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gemm_nt_tc5_kernel<PRO, EPI, NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    dim3 grid(NNP_GRID((maxM + BM - 1) / BM), (maxN + NT - 1) / NT, count);
+    gemm_nt_tc5_kernel<PRO, EPI, NT><<<grid, THREADS, smem, stream>>>(b);
+    NNP_CHECK_LAUNCH("gemm_nt_tc5");
+    return NNP_OK;
+}
+
+template <int PRO, int EPI>
+static int launch(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    int maxM = 0, maxN = 0;
+    for (int i = 0; i < count; ++i) {
+        maxM = std::max(maxM, b.g[i].M);
+        maxN = std::max(maxN, b.g[i].N);
+        if (b.g[i].N != b.g[0].N) {
+            nnp_set_error("tc5 gemm: batched problems must share N");
+            return NNP_ERR_INVALID;
+        }
+    }
+    if (maxM <= 0) return NNP_OK;
+    if (maxN % 128 == 0) return launch_nt<PRO, EPI, 128>(b, count, maxM, maxN, stream);
+    if (maxN % 64 == 0) return launch_nt<PRO, EPI, 64>(b, count, maxM, maxN, stream);
+    if (maxN % 32 == 0) return launch_nt<PRO, EPI, 32>(b, count, maxM, maxN, stream);
+    if (maxN % 16 == 0) return launch_nt<PRO, EPI, 16>(b, count, maxM, maxN, stream);
+    return -100;   // shape not covered: caller falls back to the mma.sync tile
+}
+
+}  // namespace tc5
+
+template <int PRO, int EPI>
+static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    int maxM = 0, maxN = 0;
+    for (int i = 0; i < count; ++i) {
+        maxM = b.g[i].M > maxM ? b.g[i].M : maxM;
+        maxN = b.g[i].N > maxN ? b.g[i].N : maxN;
+        if (b.g[i].K % 4 != 0 || b.g[i].lda % 4 != 0) {
+            nnp_set_error("gemm: K=%d and lda=%d must be multiples of 4", b.g[i].K, b.g[i].lda);
+            return NNP_ERR_INVALID;
+        }
+    }
+    if (maxM <= 0) return NNP_OK;
+    if (g_nnp_gemm_use_mma == 2) {
+        int rc = tc5::launch<PRO, EPI>(b, count, stream);
+        if (rc != -100) return rc;
+    }
+    dim3 grid(NNP_GRID((maxM + GEMM_BM - 1) / GEMM_BM), (maxN + GEMM_BN - 1) / GEMM_BN, count);
+    if (g_nnp_gemm_use_mma)
+        gemm_nt_kernel<PRO, EPI, true><<<grid, GEMM_THREADS, 0, stream>>>(b);
+    else
+        gemm_nt_kernel<PRO, EPI, false><<<grid, GEMM_THREADS, 0, stream>>>(b);
+    NNP_CHECK_LAUNCH("gemm_nt");
+    return NNP_OK;
+}

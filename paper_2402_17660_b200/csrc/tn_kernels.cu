@@ -14,13 +14,15 @@
 // from per-layer cubic-Hermite tables in u = exp(cutoff_lower - d), built by the host in
 // float64: they depend on the distance only, so tabulating them removes the per-edge MLP
 // (135k MAC/edge/layer) from both the forward and the force pass.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "nnp_common.cuh"
-#include "tn_gemm.cuh"
+#include "tn_gemm_tc5.cuh"
 #include "tn_math.cuh"
 
-int g_nnp_gemm_use_mma = 1;
+int g_nnp_gemm_use_mma = 2;  // 2 = tcgen05 3xTF32 (default), 1 = mma.sync 3xTF32, 0 = FP32 FFMA
 
 namespace {
 
@@ -57,9 +59,12 @@ __device__ __forceinline__ void stv(float *p, const float (&v)[CPL])
     }
 }
 
+constexpr int NNP_PARTS = 4;  // max channel parts a node's row is split over (C / (32 * CPL))
+
 struct TnDev {
     nnp_tn_model m;
     int n, n_samples, capacity;
+    int nparts;  // channel-part slots of g_d / g_u in use this step (<= NNP_PARTS)
     // inputs
     const int *species, *batch, *order, *row_ptr, *pairs, *nl_counts;
     const float *deltas, *dists;
@@ -69,8 +74,8 @@ struct TnDev {
     int *col;
     float4 *geoA;  // (table coordinate, phi, dphi/dd, 1/d)
     float4 *geoB;  // (ux, uy, uz, u = exp(cutoff_lower - d))
-    float *g_d;
-    float4 *g_u;
+    float *g_d;    // [NNP_PARTS][capacity] dE/dd_e, one slot per channel part (summed in k_forces)
+    float4 *g_u;   // [NNP_PARTS][capacity] dE/du_e
     // workspace: nodes
     int *zs, *sample_ptr;
     float *X0, *n0, *ln0, *e0, *e1, *Xm, *Xa, *Xb;
@@ -129,19 +134,21 @@ __global__ void k_edge_geom(TnDev d)
     d.geoA[e] = make_float4(tx, phi, dphi, invd);
     d.geoB[e] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
                             d.deltas[3 * (size_t)e + 2] * invd, u);
-    d.g_d[e] = 0.0f;
-    d.g_u[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < d.nparts; ++p) {
+        d.g_d[(size_t)p * d.capacity + e] = 0.0f;
+        d.g_u[(size_t)p * d.capacity + e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 }
 
 // Hermite lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coord).
 template <int C, int CPL, bool DERIV>
 __device__ __forceinline__ void table_lookup(const float *__restrict__ tab, int num_knots, float tx,
-                                             int lane, float (&f)[3][CPL], float (&df)[3][CPL])
+                                             int cb, float (&f)[3][CPL], float (&df)[3][CPL])
 {
     int kn = (int)tx;
     kn = kn > num_knots - 2 ? num_knots - 2 : kn;
     const Hermite h = hermite_weights(tx - (float)kn);
-    const float *row0 = tab + (size_t)kn * (6 * C) + lane * CPL;
+    const float *row0 = tab + (size_t)kn * (6 * C) + cb;
     const float *row1 = row0 + 6 * C;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -163,15 +170,16 @@ __device__ __forceinline__ int group_of(int q) { return q == 0 ? 0 : (q < 4 ? 1 
 // ----------------------------------------------------------------------------- embedding
 // X0_i = sum_e w_e[:,grp] * basis_e  with w_e = dp(rho_e) * phi_e * Z_e ; then n0 = |X0|^2 and
 // ln0 = LayerNorm_C(n0).
-template <int C>
+template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
 {
-    constexpr int CPL = C / 32;
+    constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
-    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
-    const int cb = lane * CPL;
+    const int cb = part * 32 * CPL + lane * CPL;
     float zr[CPL];
     ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
     float acc[9][CPL];
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
         float zsnd[CPL];
         ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, false>(d.m.tables, d.m.num_knots, ga.x, lane, f, df);
+        table_lookup<C, CPL, false>(d.m.tables, d.m.num_knots, ga.x, cb, f, df);
         float b[9];
         edge_basis9(gb.x, gb.y, gb.z, b);
 #pragma unroll
@@ -203,18 +211,32 @@ __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
         }
     }
     float nrm[CPL];
-    float sum = 0.0f;
 #pragma unroll
     for (int v = 0; v < CPL; ++v) {
         float c9[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) c9[q] = acc[q][v];
         nrm[v] = c9_frob(c9, c9);
-        sum += nrm[v];
     }
 #pragma unroll
     for (int q = 0; q < 9; ++q) stv<CPL>(d.X0 + ((size_t)s * 9 + q) * C + cb, acc[q]);
     stv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+}
+
+// ln0 = LayerNorm_C(n0): one warp per node over all channels
+template <int C>
+__global__ void __launch_bounds__(256) k_embed_ln(TnDev d)
+{
+    constexpr int CPL = C / 32;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int cb = lane * CPL;
+    float nrm[CPL];
+    ldv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+    float sum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) sum += nrm[v];
     const float mean = nnp_warp_sum(sum) * (1.0f / C);
     float var = 0.0f;
 #pragma unroll
@@ -353,15 +375,16 @@ __global__ void k_embed_gate_bwd(const float *__restrict__ GX, const float *__re
 
 // ----------------------------------------------------------------------- interaction edges
 // M_i = sum_e f_e[:,grp] * Yc_j   (f_e = table(u_e) * phi_e)
-template <int C>
+template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
 {
-    constexpr int CPL = C / 32;
+    constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
-    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
-    const int cb = lane * CPL;
+    const int cb = part * 32 * CPL + lane * CPL;
     const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
     const float *Y = d.Yc[layer];
     float acc[9][CPL];
@@ -374,7 +397,7 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
         const int j = d.col[e];
         const float4 ga = d.geoA[e];
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, false>(tab, d.m.num_knots, ga.x, lane, f, df);
+        table_lookup<C, CPL, false>(tab, d.m.num_knots, ga.x, cb, f, df);
         const float *yj = Y + (size_t)j * 9 * C + cb;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
@@ -388,22 +411,43 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
     float *out = d.Mc[layer] + (size_t)s * 9 * C + cb;
 #pragma unroll
     for (int q = 0; q < 9; ++q) stv<CPL>(out + q * C, acc[q]);
+    // node update fused in: Q = (M*Y + Y*M) / (|M*Y + Y*M|^2 + 1) for this node's channels
+    const float *yi = Y + (size_t)s * 9 * C + cb;
+    float yown[9][CPL], qv[9][CPL];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ldv<CPL>(yi + q * C, yown[q]);
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float m9[9], y9[9], q9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            m9[q] = acc[q][v];
+            y9[q] = yown[q][v];
+        }
+        node_product_fwd(m9, y9, q9);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) qv[q][v] = q9[q];
+    }
+    float *qo = d.Qc + (size_t)s * 9 * C + cb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<CPL>(qo + q * C, qv[q]);
 }
 
 // Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
 // is a gather over a's own row):
 //   G_Y[a] += sum_e f_e[:,grp] * G_M[b]              (b = sender of e)
 //   g_d[e] += sum_c sum_k <G_M[a], Yc[b]>_k * d f_e[c,k] / dd
-template <int C>
+template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
                                                           float *GY)
 {
-    constexpr int CPL = C / 32;
+    constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
-    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
-    const int cb = lane * CPL;
+    const int cb = part * 32 * CPL + lane * CPL;
     const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
     const float *Y = d.Yc[layer];
     float gma[9][CPL], acc[9][CPL];
@@ -423,7 +467,7 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
         const float4 ga = d.geoA[e];
         const float u = d.geoB[e].w;
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, true>(tab, d.m.num_knots, ga.x, lane, f, df);
+        table_lookup<C, CPL, true>(tab, d.m.num_knots, ga.x, cb, f, df);
         const float *gj = GM + (size_t)j * 9 * C + cb;
         const float *yj = Y + (size_t)j * 9 * C + cb;
         float gf[3][CPL];
@@ -437,7 +481,7 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
             ldv<CPL>(gj + q * C, gmj[q]);
             ldv<CPL>(yj + q * C, yv[q]);
         }
-        float part = 0.0f;
+        float psum = 0.0f;
 #pragma unroll
         for (int v = 0; v < CPL; ++v) {
             float a9[9], y9[9];
@@ -450,11 +494,11 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
             const float gI = c9_dot_I(a9, y9), gA = c9_dot_A(a9, y9), gS = c9_dot_S(a9, y9);
             // d f_e/dd = phi * d f~/dd + f~ * dphi ;  d f~/dd = -u * (d f~/dt) / u_step
             const float su = -u * inv_step * ga.y;
-            part += gI * (df[0][v] * su + f[0][v] * ga.z) + gA * (df[1][v] * su + f[1][v] * ga.z) +
+            psum += gI * (df[0][v] * su + f[0][v] * ga.z) + gA * (df[1][v] * su + f[1][v] * ga.z) +
                     gS * (df[2][v] * su + f[2][v] * ga.z);
         }
-        part = nnp_warp_sum(part);
-        if (lane == 0 && j != s) d.g_d[e] += part;
+        psum = nnp_warp_sum(psum);
+        if (lane == 0 && j != s) d.g_d[(size_t)part * d.capacity + e] += psum;
     }
     float *out = GY + (size_t)s * 9 * C + cb;
 #pragma unroll
@@ -668,15 +712,16 @@ __global__ void __launch_bounds__(256) k_embed_norm_bwd(TnDev d, float *GX0)
 }
 
 // reverse of k_embed_edge: per edge g_d += dE/dd (through dp(rho) and phi) and g_u = dE/du
-template <int C>
+template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX0)
 {
-    constexpr int CPL = C / 32;
+    constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
-    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
-    const int cb = lane * CPL;
+    const int cb = part * 32 * CPL + lane * CPL;
     float zr[CPL];
     ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
     float G[9][CPL];
@@ -693,7 +738,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         float zsnd[CPL];
         ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, true>(d.m.tables, d.m.num_knots, ga.x, lane, f, df);
+        table_lookup<C, CPL, true>(d.m.tables, d.m.num_knots, ga.x, cb, f, df);
         float b[9];
         edge_basis9(gb.x, gb.y, gb.z, b);
         const float su = -gb.w * inv_step * ga.y;
@@ -720,8 +765,8 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         py = nnp_warp_sum(py);
         pz = nnp_warp_sum(pz);
         if (lane == 0) {
-            d.g_d[e] += pd;
-            d.g_u[e] = make_float4(px, py, pz, 0.0f);
+            d.g_d[(size_t)part * d.capacity + e] += pd;
+            d.g_u[(size_t)part * d.capacity + e] = make_float4(px, py, pz, 0.0f);
         }
     }
 }
@@ -746,9 +791,15 @@ __global__ void k_forces(TnDev d)
         const int er = lo;
         const float4 ga = d.geoA[e];
         const float4 gb = d.geoB[e];
-        const float4 ue = d.g_u[e], ur = d.g_u[er];
-        const float gd = d.g_d[e] + d.g_d[er];
-        const float vx = ue.x - ur.x, vy = ue.y - ur.y, vz = ue.z - ur.z;
+        float gd = 0.0f, vx = 0.0f, vy = 0.0f, vz = 0.0f;
+        for (int p = 0; p < d.nparts; ++p) {
+            const size_t po = (size_t)p * d.capacity;
+            const float4 ue = d.g_u[po + e], ur = d.g_u[po + er];
+            gd += d.g_d[po + e] + d.g_d[po + er];
+            vx += ue.x - ur.x;
+            vy += ue.y - ur.y;
+            vz += ue.z - ur.z;
+        }
         const float dot = vx * gb.x + vy * gb.y + vz * gb.z;
         gx += gd * gb.x + (vx - gb.x * dot) * ga.w;
         gy += gd * gb.y + (vy - gb.y * dot) * ga.w;
@@ -776,8 +827,8 @@ size_t carve(TnDev &d, void *ws)
     d.col = ar.take<int>(cap);
     d.geoA = ar.take<float4>(cap);
     d.geoB = ar.take<float4>(cap);
-    d.g_d = ar.take<float>(cap);
-    d.g_u = ar.take<float4>(cap);
+    d.g_d = ar.take<float>(cap * NNP_PARTS);
+    d.g_u = ar.take<float4>(cap * NNP_PARTS);
     d.zs = ar.take<int>(n);
     d.sample_ptr = ar.take<int>((size_t)d.n_samples + 1);
     d.X0 = ar.take<float>(T);
@@ -868,6 +919,37 @@ GemmBatch mix_gemm(const float *A, const float *W3, float *out, int n, int C, fl
     return b;
 }
 
+// Channels per lane of the four row-walking edge kernels (1, 2 or 4; C / (32 * CPL) warps share a
+// node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
+// through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
+struct EdgeTuning {
+    int emb, fwd, bwd, embbwd;
+};
+static int env_int(const char *name, int fallback)
+{
+    const char *v = getenv(name);
+    return v ? atoi(v) : fallback;
+}
+static const EdgeTuning &edge_tuning()
+{
+    static const EdgeTuning t = {env_int("NNP_CPL_EMB", 2), env_int("NNP_CPL_FWD", 4),
+                                 env_int("NNP_CPL_BWD", 2), env_int("NNP_CPL_EMBBWD", 4)};
+    return t;
+}
+#define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
+    do {                                                          \
+        int cpl__ = (cpl_req);                                    \
+        if (cpl__ * 32 > (C)) cpl__ = (C) / 32;                   \
+        if (cpl__ != 1 && cpl__ != 2 && cpl__ != 4) cpl__ = 1;    \
+        if (cpl__ == 4) {                                         \
+            if constexpr ((C) >= 128) { constexpr int CPL = 4; LAUNCH; } \
+        } else if (cpl__ == 2) {                                  \
+            if constexpr ((C) >= 64) { constexpr int CPL = 2; LAUNCH; }  \
+        } else {                                                  \
+            constexpr int CPL = 1; LAUNCH;                        \
+        }                                                         \
+    } while (0)
+
 template <int C>
 int run_step(TnDev &d, cudaStream_t st)
 {
@@ -875,6 +957,15 @@ int run_step(TnDev &d, cudaStream_t st)
     const int warp_blocks = nnp_blocks(n, 8);
     const int ew_blocks = nnp_blocks((int64_t)n * C, 256);
     const nnp_tn_model &m = d.m;
+    const EdgeTuning &tune = edge_tuning();
+    {
+        auto parts = [](int cpl) {
+            if (cpl * 32 > C) cpl = C / 32;
+            if (cpl != 1 && cpl != 2 && cpl != 4) cpl = 1;
+            return C / (32 * cpl);
+        };
+        d.nparts = std::max(parts(tune.bwd), parts(tune.embbwd));
+    }
     int rc;
 #define RUN(x)            \
     do {                  \
@@ -887,7 +978,8 @@ int run_step(TnDev &d, cudaStream_t st)
     { NNP_PROF("k_edge_geom", st); k_edge_geom<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
 
     // ---- embedding
-    { NNP_PROF("k_embed_edge", st); k_embed_edge<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
+    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d))); }
+    { NNP_PROF("k_embed_ln", st); k_embed_ln<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.ln0, m.es0_w, m.es0_b, d.e0, n, 2 * C, C);
@@ -904,8 +996,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
-        { NNP_PROF("k_edge_message", st); k_edge_message<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, l); }
-        { NNP_PROF("k_node_product", st); k_node_product<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], d.Qc, n, C); }
+        { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, l))); }
         GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + (size_t)3 * C * C, d.Dc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
         { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, n, C); }
@@ -947,7 +1038,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        { NNP_PROF("k_edge_message_bwd", st); k_edge_message_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, l, Ga, d.Qc); }
+        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, l, Ga, d.Qc))); }
         // G_Xh = GX + mix^T(G_Y)  -> written in place over GX
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GX, n, C, nullptr, GX, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st))); }
@@ -967,7 +1058,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
     { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
-    { NNP_PROF("k_embed_edge_bwd", st); k_embed_edge_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
+    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, Gb))); }
     { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(nnp_blocks(n, 128)), 128, 0, st>>>(d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
@@ -1041,7 +1132,7 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = use_mma ? 1 : 0;
+    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 2 ? 2 : use_mma);
     return NNP_OK;
 }
 

@@ -49,13 +49,14 @@ def check(model, z, pos, batch, box, e_tol=E_TOL, f_tol=F_TOL):
     return e_err, f_err
 
 
-@pytest.mark.parametrize("mode", [1, 0])
+@pytest.mark.parametrize("mode", [2, 1, 0])
 def test_gemm_tile_engine(mode):
     lib = _lib.load()
     lib.nnp_set_gemm_mode(mode)
     try:
         g = torch.Generator(device="cuda").manual_seed(0)
-        for M, N, K in [(64, 64, 32), (200, 128, 128), (333, 384, 256), (70, 16, 64), (129, 96, 16)]:
+        for M, N, K in [(64, 64, 32), (200, 128, 128), (333, 384, 256), (70, 16, 64), (129, 96, 16),
+                        (1000, 256, 128), (5000, 128, 64), (128, 32, 384)]:
             A = torch.randn(M, K, device="cuda", generator=g)
             W = torch.randn(N, K, device="cuda", generator=g)
             bias = torch.randn(N, device="cuda", generator=g)
@@ -65,7 +66,7 @@ def test_gemm_tile_engine(mode):
             assert rc == 0
             ref = (A.double() @ W.double().T + bias.double())
             err = (out.double() - ref).abs().max().item() / ref.abs().max().item()
-            assert err < 2e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
+            assert err < 5e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
     finally:
         lib.nnp_set_gemm_mode(1)
 
@@ -86,7 +87,7 @@ def test_small_open_system(rng, C, L):
     check(model, *small_open(rng))
 
 
-@pytest.mark.parametrize("gemm_mode", [1, 0])
+@pytest.mark.parametrize("gemm_mode", [2, 1, 0])
 def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
     _lib.load().nnp_set_gemm_mode(gemm_mode)
     try:
