@@ -113,22 +113,4 @@ def config_e_triclinic(n: int = 100_000, seed: int = 3, min_sep: float = 0.0):
     return species, _f32(pos), np.zeros(n, dtype=np.int64), box
 
 
-def shard_by_molecule(batch: np.ndarray, world_size: int):
-    """Contiguous molecule ranges balanced on atom count: returns, per rank,
-    (atom_start, atom_end, sample_start, sample_end)."""
-    batch = np.asarray(batch)
-    n_samples = int(batch[-1]) + 1
-    sizes = np.bincount(batch, minlength=n_samples)
-    cum = np.concatenate([[0], np.cumsum(sizes)])
-    total = cum[-1]
-    shards = []
-    s0 = 0
-    for r in range(world_size):
-        target = total * (r + 1) / world_size
-        s1 = int(np.searchsorted(cum, target, side="left")) if r < world_size - 1 else n_samples
-        s1 = max(s1, s0 + (1 if s0 < n_samples else 0))
-        s1 = min(s1, n_samples - (world_size - 1 - r)) if n_samples >= world_size else min(s1, n_samples)
-        s1 = max(s1, s0)
-        shards.append((int(cum[s0]), int(cum[s1]), s0, s1))
-        s0 = s1
-    return shards
+from .sharding import shard_by_molecule  # noqa: E402,F401  (kept importable from here)

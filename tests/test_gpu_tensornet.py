@@ -68,7 +68,7 @@ def test_gemm_tile_engine(mode):
             err = (out.double() - ref).abs().max().item() / ref.abs().max().item()
             assert err < 5e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
     finally:
-        lib.nnp_set_gemm_mode(1)
+        lib.nnp_set_gemm_mode(2)
 
 
 def small_open(rng, n=20):
@@ -101,7 +101,7 @@ def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
                             cutoff_upper=4.5, max_z=10, seed=6)
         check(model, z, pos, None, box)
     finally:
-        _lib.load().nnp_set_gemm_mode(1)
+        _lib.load().nnp_set_gemm_mode(2)
 
 
 def test_config_a_alanine_sized_molecule():
