@@ -113,6 +113,14 @@ int nnp_distance_pullback(const int32_t *pairs, const double *deltas, const doub
  */
 #define NNP_TN_MAX_LAYERS 8
 
+/* A GEMM weight W[N,K] (row-major float32) plus, for the tcgen05 path, its TF32 hi/lo split
+ * pre-arranged as shared-memory tile images: [N/NT][ceil(K/32)][NT rows][32 floats], each row's
+ * eight 16-byte chunks XOR-swizzled by (row % 8) (the K-major SWIZZLE_128B operand layout), NT =
+ * 128/64/32/16 = the largest of these dividing N.  hi/lo may be NULL (slower generic path). */
+typedef struct nnp_gemm_weight {
+    const float *w, *hi, *lo;
+} nnp_gemm_weight;
+
 typedef struct nnp_tn_model {
     int32_t channels;  /* C: 32, 64 or 128 (GNConfig.embedding_dimension, graphnet.py:59) */
     int32_t num_rbf;   /* K (only used by the host when it builds the tables) */
@@ -126,19 +134,21 @@ typedef struct nnp_tn_model {
     /* species tables: Z_e = z_recv[z_i] + z_send[z_j]  (emb2 bias folded into z_send) */
     const float *z_recv; /* [max_z, C] */
     const float *z_send; /* [max_z, C] */
-    /* radial tables [(L+1)][num_knots][2][3][C]: table 0 = distance projections dp1..3 of the
-       embedding, table 1+l = radial MLP of layer l (before the cosine envelope);
-       [..][0] = value, [..][1] = u_step * d(value)/du */
+    /* radial tables [(L+1)][num_knots-1][4][3][C]: table 0 = distance projections dp1..3 of the
+       embedding, table 1+l = radial MLP of layer l (before the cosine envelope); per knot interval
+       the monomial coefficients c0..c3 of the cubic Hermite interpolant in x = (u-u_k)/u_step */
     const float *tables;
     const float *init_norm_g, *init_norm_b;             /* [C] */
-    const float *es0_w, *es0_wT, *es0_b;                /* [2C,C], [C,2C], [2C] */
-    const float *es1_w, *es1_wT, *es1_b;                /* [3C,2C], [2C,3C], [3C] */
-    const float *et_w, *et_wT;                          /* [3,C,C] each */
-    const float *layer_t_w[NNP_TN_MAX_LAYERS];          /* [6,C,C] */
-    const float *layer_t_wT[NNP_TN_MAX_LAYERS];         /* [6,C,C] transposed */
+    nnp_gemm_weight es0_w, es0_wT;                      /* [2C,C], [C,2C] */
+    nnp_gemm_weight es1_w, es1_wT;                      /* [3C,2C], [2C,3C] */
+    const float *es0_b, *es1_b;                         /* [2C], [3C] */
+    nnp_gemm_weight et_w[3], et_wT[3];                  /* [C,C] each (I, A, S mixes) */
+    nnp_gemm_weight layer_t_w[NNP_TN_MAX_LAYERS][6];    /* [C,C] each: lt0..lt5 */
+    nnp_gemm_weight layer_t_wT[NNP_TN_MAX_LAYERS][6];   /* transposes (reverse sweep) */
     const float *out_norm_g, *out_norm_b;               /* [3C] */
-    const float *lin_w, *lin_wT, *lin_b;                /* [C,3C], [3C,C], [C] */
-    const float *h1_w, *h1_wT, *h1_b;                   /* [C/2,C], [C,C/2], [C/2] */
+    nnp_gemm_weight lin_w, lin_wT;                      /* [C,3C], [3C,C] */
+    nnp_gemm_weight h1_w, h1_wT;                        /* [C/2,C], [C,C/2] */
+    const float *lin_b, *h1_b;                          /* [C], [C/2] */
     const float *h2_w;                                  /* [C/2] */
 } nnp_tn_model;
 
@@ -166,9 +176,10 @@ int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_sampl
 
 /* Test hook: out[M,N] = A[M,K] * W[N,K]^T (+ bias[N]) through the same tile engine the node
  * kernels use (3xTF32 tensor-core path or FP32 FFMA). */
-int nnp_test_gemm_nt(const float *A, const float *W, const float *bias, float *out, int32_t M,
-                     int32_t N, int32_t K, nnp_stream_t stream);
-/* Test hook: 1 = 3xTF32 tensor-core inner loop (default), 0 = FP32 FFMA inner loop. */
+int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const float *bias, float *out,
+                     int32_t M, int32_t N, int32_t K, nnp_stream_t stream);
+/* Test hook: 3 = tcgen05 3xTF32, one tile per CTA (default), 2 = persistent warp-specialised
+ * tcgen05, 1 = mma.sync 3xTF32, 0 = FP32 FFMA inner loop. */
 int nnp_set_gemm_mode(int use_mma);
 
 /* Instrumentation (bench.py / tests): number of kernels this library has enqueued so far

@@ -44,6 +44,10 @@ class NlParams(ctypes.Structure):
     ]
 
 
+class GemmWeight(ctypes.Structure):
+    _fields_ = [("w", _p), ("hi", _p), ("lo", _p)]
+
+
 class TnModel(ctypes.Structure):
     _fields_ = [
         ("channels", _i32), ("num_rbf", _i32), ("num_layers", _i32), ("max_z", _i32),
@@ -52,13 +56,16 @@ class TnModel(ctypes.Structure):
         ("mean", _f), ("std", _f), ("h2_b", _f),
         ("z_recv", _p), ("z_send", _p), ("tables", _p),
         ("init_norm_g", _p), ("init_norm_b", _p),
-        ("es0_w", _p), ("es0_wT", _p), ("es0_b", _p),
-        ("es1_w", _p), ("es1_wT", _p), ("es1_b", _p),
-        ("et_w", _p), ("et_wT", _p),
-        ("layer_t_w", _p * TN_MAX_LAYERS), ("layer_t_wT", _p * TN_MAX_LAYERS),
+        ("es0_w", GemmWeight), ("es0_wT", GemmWeight),
+        ("es1_w", GemmWeight), ("es1_wT", GemmWeight),
+        ("es0_b", _p), ("es1_b", _p),
+        ("et_w", GemmWeight * 3), ("et_wT", GemmWeight * 3),
+        ("layer_t_w", (GemmWeight * 6) * TN_MAX_LAYERS),
+        ("layer_t_wT", (GemmWeight * 6) * TN_MAX_LAYERS),
         ("out_norm_g", _p), ("out_norm_b", _p),
-        ("lin_w", _p), ("lin_wT", _p), ("lin_b", _p),
-        ("h1_w", _p), ("h1_wT", _p), ("h1_b", _p),
+        ("lin_w", GemmWeight), ("lin_wT", GemmWeight),
+        ("h1_w", GemmWeight), ("h1_wT", GemmWeight),
+        ("lin_b", _p), ("h1_b", _p),
         ("h2_w", _p),
     ]
 
@@ -93,7 +100,7 @@ def load() -> ctypes.CDLL:
     lib.nnp_tn_energy_forces.argtypes = [
         ctypes.POINTER(TnModel), _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, sz, _p,
     ]
-    lib.nnp_test_gemm_nt.argtypes = [_p, _p, _p, _p, _i32, _i32, _i32, _p]
+    lib.nnp_test_gemm_nt.argtypes = [_p, ctypes.POINTER(GemmWeight), _p, _p, _i32, _i32, _i32, _p]
     lib.nnp_set_gemm_mode.argtypes = [ctypes.c_int]
     lib.nnp_launch_count.argtypes = [ctypes.c_int]
     lib.nnp_profile_begin.argtypes = []

@@ -20,6 +20,7 @@ enum { EPI_STORE = 0, EPI_MUL_SILU_GRAD = 1, EPI_GATE = 2, EPI_ADD = 3 };
 struct GemmArgs {
     const float *A;
     const float *W;
+    const float *Whi, *Wlo;  // TF32 hi/lo tile images of W (tensornet.stage_gemm_weight) or NULL
     const float *bias;
     float *out;
     float *out2;
@@ -245,4 +246,5 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
     }
 }
 
-extern int g_nnp_gemm_use_mma;  // 2 = tcgen05 3xTF32 (default), 1 = mma.sync 3xTF32, 0 = FP32 FFMA
+extern int g_nnp_gemm_use_mma;  // 3 = tcgen05 3xTF32, one tile per CTA, 3 CTAs/SM (default);
+                                // 2 = persistent warp-specialised tcgen05; 1 = mma.sync 3xTF32; 0 = FP32 FFMA

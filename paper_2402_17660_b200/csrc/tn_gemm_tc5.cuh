@@ -273,6 +273,278 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Persistent, warp-specialised version (the one the model step uses).  One CTA per SM loops over
+// output tiles; three roles run concurrently and meet only through mbarriers:
+//   warps 4-7  producers : A rows global -> registers -> TF32 hi/lo split -> swizzled smem stage
+//   warp  8    (1 thread): bulk-copies (cp.async.bulk, complete_tx on the stage's "full" barrier)
+//                          the pre-split, pre-swizzled weight chunk images, then issues the
+//                          tcgen05.mma triple per K step and commits to "empty" / "tmem_full"
+//   warps 0-3  epilogue  : tcgen05.ld of the finished accumulator -> swizzled smem staging tile ->
+//                          coalesced float4 global stores with the fused epilogue
+// Two operand stages and two TMEM accumulators let the loads of chunk c+1, the MMAs of chunk c
+// and the epilogue of the previous tile overlap.  Weights are split/swizzled once on the host
+// (tensornet.stage_gemm_weight), so the per-tile producer work is the activation tile only.
+constexpr int WS_THREADS = 288;
+constexpr int WS_STAGES = 2;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct TileCoord {
+    int z, m0, nt_idx;
+};
+
+__device__ __forceinline__ bool decode_tile(const GemmBatch &b, int count, int n_tiles_n, int tile,
+                                            TileCoord &tc)
+{
+    for (int z = 0; z < count; ++z) {
+        const int tm = (b.g[z].M + BM - 1) / BM;
+        const int tz = tm * n_tiles_n;
+        if (tile < tz) {
+            tc.z = z;
+            tc.m0 = (tile / n_tiles_n) * BM;
+            tc.nt_idx = tile % n_tiles_n;
+            return true;
+        }
+        tile -= tz;
+    }
+    return false;
+}
+
+template <int PRO, int EPI, int NT>
+__global__ void __launch_bounds__(WS_THREADS, 1) gemm_tc5_ws_kernel(GemmBatch batch, int count,
+                                                                   int total_tiles, int n_tiles_n)
+{
+    constexpr int TMEM_COLS = (2 * NT) <= 32 ? 32 : ((2 * NT) <= 64 ? 64 : ((2 * NT) <= 128 ? 128 : 256));
+    constexpr int A_PASSES = BM / 16;
+    constexpr int STAGE_BYTES = 2 * BM * 128 + 2 * NT * 128;
+    constexpr int CH = NT / 4;
+
+    extern __shared__ char smem_raw[];
+    char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    float *stage_out = reinterpret_cast<float *>(smem + WS_STAGES * STAGE_BYTES);
+    __shared__ uint64_t full_bar[WS_STAGES], empty_bar[WS_STAGES], tfull_bar[2], tempty_bar[2];
+    __shared__ uint32_t tmem_base_s;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < WS_STAGES; ++s) {
+            mbar_init(&full_bar[s], 128 + 1);   // 128 producer threads + the expect_tx arrival
+            mbar_init(&empty_bar[s], 1);        // tcgen05.commit
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull_bar[a], 1);        // tcgen05.commit
+            mbar_init(&tempty_bar[a], 128);     // epilogue threads
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "n"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = tmem_base_s;
+
+    if (warp >= 4 && warp < 8) {
+        // ===================================================================== producers
+        const int ptid = tid - 128;
+        const int lrow = ptid >> 3, lchunk = ptid & 7;
+        int it = 0;   // running chunk counter -> stage and phase
+        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            TileCoord tc;
+            decode_tile(batch, count, n_tiles_n, tile, tc);
+            const GemmArgs &g = batch.g[tc.z];
+            const int nchunks = (g.K + KC - 1) / KC;
+            const float *a_ptr[A_PASSES];
+#pragma unroll
+            for (int p = 0; p < A_PASSES; ++p) {
+                const int r = tc.m0 + p * 16 + lrow;
+                a_ptr[p] = r < g.M ? g.A + (size_t)gemm_phys_row(g, r) * g.lda + lchunk * 4 : nullptr;
+            }
+            float4 ra[A_PASSES];
+            auto load_chunk = [&](int c) {
+                const int k0 = c * KC;
+                const bool k_ok = k0 + lchunk * 4 < g.K;
+#pragma unroll
+                for (int p = 0; p < A_PASSES; ++p) {
+                    ra[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (a_ptr[p] && k_ok) ra[p] = __ldg(reinterpret_cast<const float4 *>(a_ptr[p] + k0));
+                }
+            };
+            load_chunk(0);
+            for (int c = 0; c < nchunks; ++c, ++it) {
+                const int s = it % WS_STAGES;
+                const uint32_t ph = (uint32_t)((it / WS_STAGES) & 1);
+                mbar_wait(&empty_bar[s], ph ^ 1);          // stage free (passes at once the first time)
+                char *a_hi = smem + s * STAGE_BYTES, *a_lo = a_hi + BM * 128;
+#pragma unroll
+                for (int p = 0; p < A_PASSES; ++p) {
+                    float4 v = ra[p];
+                    if (PRO == PRO_SILU) {
+                        v.x = nnp_silu(v.x);
+                        v.y = nnp_silu(v.y);
+                        v.z = nnp_silu(v.z);
+                        v.w = nnp_silu(v.w);
+                    }
+                    split_store(a_hi, a_lo, swz(p * 16 + lrow, lchunk), v);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&full_bar[s]);
+                if (c + 1 < nchunks) load_chunk(c + 1);
+            }
+        }
+    } else if (warp == 8) {
+        // ===================================================== weight copies + MMA issue (1 thread)
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(NT);
+            int it = 0, tcount = 0;
+            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++tcount) {
+                TileCoord tc;
+                decode_tile(batch, count, n_tiles_n, tile, tc);
+                const GemmArgs &g = batch.g[tc.z];
+                const int nchunks = (g.K + KC - 1) / KC;
+                const int acc = tcount & 1;
+                const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+                mbar_wait(&tempty_bar[acc], acc_ph ^ 1);   // epilogue has drained this accumulator
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t tmem_d = tmem_base + (uint32_t)(acc * NT);
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = it % WS_STAGES;
+                    const uint32_t ph = (uint32_t)((it / WS_STAGES) & 1);
+                    char *a_hi = smem + s * STAGE_BYTES, *a_lo = a_hi + BM * 128;
+                    char *w_hi = a_hi + 2 * BM * 128, *w_lo = w_hi + NT * 128;
+                    mbar_wait(&empty_bar[s], ph ^ 1);
+                    const size_t woff = ((size_t)tc.nt_idx * nchunks + c) * (size_t)(NT * 32);
+                    mbar_expect_tx(&full_bar[s], 2u * NT * 128u);
+                    bulk_g2s(w_hi, g.Whi + woff, NT * 128u, &full_bar[s]);
+                    bulk_g2s(w_lo, g.Wlo + woff, NT * 128u, &full_bar[s]);
+                    mbar_wait(&full_bar[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t da_hi = make_desc(smem_u32(a_hi)), da_lo = make_desc(smem_u32(a_lo));
+                    const uint64_t dw_hi = make_desc(smem_u32(w_hi)), dw_lo = make_desc(smem_u32(w_lo));
+#pragma unroll
+                    for (int ks = 0; ks < KC / 8; ++ks) {
+                        const uint64_t adv = (uint64_t)(ks * 32 >> 4);
+                        umma_tf32(tmem_d, da_lo + adv, dw_hi + adv, idesc, (c | ks) != 0);
+                        umma_tf32(tmem_d, da_hi + adv, dw_lo + adv, idesc, 1);
+                        umma_tf32(tmem_d, da_hi + adv, dw_hi + adv, idesc, 1);
+                    }
+                    umma_commit(&empty_bar[s]);                   // stage reusable when these MMAs retire
+                    if (c + 1 == nchunks) umma_commit(&tfull_bar[acc]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < 4) {
+        // ====================================================================== epilogue
+        int tcount = 0;
+        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++tcount) {
+            TileCoord tc;
+            decode_tile(batch, count, n_tiles_n, tile, tc);
+            const GemmArgs &g = batch.g[tc.z];
+            const int acc = tcount & 1;
+            const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+            mbar_wait(&tfull_bar[acc], acc_ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int rr = warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < NT; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * NT + c0), v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int pos = ((c0 >> 2) + q) ^ (rr & (CH - 1));
+                    *reinterpret_cast<float4 *>(stage_out + rr * NT + pos * 4) =
+                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty_bar[acc]);                       // accumulator may be overwritten
+            asm volatile("bar.sync 1, 128;" ::: "memory");       // staging tile complete
+            constexpr int ROWS_PER_IT = 32 / CH;
+            const int n0 = tc.nt_idx * NT;
+            for (int r0 = warp * ROWS_PER_IT; r0 < BM; r0 += 4 * ROWS_PER_IT) {
+                const int row = r0 + lane / CH;
+                const int ch = lane % CH;
+                const int pos = ch ^ (row & (CH - 1));
+                const float4 v = *reinterpret_cast<const float4 *>(stage_out + row * NT + pos * 4);
+                gemm_epilogue4<EPI>(g, tc.m0 + row, n0 + ch * 4, v);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");       // staging tile free again
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+template <int PRO, int EPI, int NT>
+static int launch_ws_nt(const GemmBatch &b, int count, int maxN, cudaStream_t stream)
+{
+    constexpr int smem = WS_STAGES * (2 * BM * 128 + 2 * NT * 128) + BM * NT * 4 + 1024;
+    static int num_sms = 0;
+    if (num_sms == 0) {
+        cudaFuncSetAttribute(gemm_tc5_ws_kernel<PRO, EPI, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    const int n_tiles_n = maxN / NT;
+    int total = 0;
+    for (int i = 0; i < count; ++i) total += ((b.g[i].M + BM - 1) / BM) * n_tiles_n;
+    if (total <= 0) return NNP_OK;
+    const int grid = total < num_sms ? total : num_sms;
+    gemm_tc5_ws_kernel<PRO, EPI, NT><<<NNP_GRID(grid), WS_THREADS, smem, stream>>>(b, count, total, n_tiles_n);
+    NNP_CHECK_LAUNCH("gemm_tc5_ws");
+    return NNP_OK;
+}
+
+// NT the host staged the weight images for (must match tensornet.gemm_tile_n)
+static inline int tile_n_for(int N) { return N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : (N % 32 == 0 ? 32 : 16)); }
+
+template <int PRO, int EPI>
+static int launch_ws(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    const int N = b.g[0].N;
+    for (int i = 0; i < count; ++i)
+        if (b.g[i].N != N || !b.g[i].Whi || !b.g[i].Wlo || N % 16 != 0) return -100;
+    switch (tile_n_for(N)) {
+    case 128: return launch_ws_nt<PRO, EPI, 128>(b, count, N, stream);
+    case 64: return launch_ws_nt<PRO, EPI, 64>(b, count, N, stream);
+    case 32: return launch_ws_nt<PRO, EPI, 32>(b, count, N, stream);
+    default: return launch_ws_nt<PRO, EPI, 16>(b, count, N, stream);
+    }
+}
+
 template <int PRO, int EPI, int NT>
 static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStream_t stream)
 {
@@ -324,8 +596,9 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
         }
     }
     if (maxM <= 0) return NNP_OK;
-    if (g_nnp_gemm_use_mma == 2) {
-        int rc = tc5::launch<PRO, EPI>(b, count, stream);
+    if (g_nnp_gemm_use_mma >= 2) {
+        int rc = g_nnp_gemm_use_mma == 2 ? tc5::launch_ws<PRO, EPI>(b, count, stream) : -100;
+        if (rc == -100) rc = tc5::launch<PRO, EPI>(b, count, stream);
         if (rc != -100) return rc;
     }
     dim3 grid(NNP_GRID((maxM + GEMM_BM - 1) / GEMM_BM), (maxN + GEMM_BN - 1) / GEMM_BN, count);

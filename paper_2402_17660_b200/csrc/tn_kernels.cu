@@ -22,7 +22,7 @@
 #include "tn_gemm_tc5.cuh"
 #include "tn_math.cuh"
 
-int g_nnp_gemm_use_mma = 2;  // 2 = tcgen05 3xTF32 (default), 1 = mma.sync 3xTF32, 0 = FP32 FFMA
+int g_nnp_gemm_use_mma = 3;  // 3 = tcgen05 one tile per CTA (default), 2 = persistent tcgen05, 1 = mma.sync, 0 = FFMA
 
 namespace {
 
@@ -140,28 +140,48 @@ __global__ void k_edge_geom(TnDev d)
     }
 }
 
-// Hermite lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coord).
+// Lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coordinate).
+// The host stores, per knot interval, the cubic's monomial coefficients [c0 c1 c2 c3][3][C]
+// (the Hermite interpolant of values and slopes, expanded in float64), so the device evaluates
+// by Horner: f = ((c3 t + c2) t + c1) t + c0,  f' = (3 c3 t + 2 c2) t + c1.
 template <int C, int CPL, bool DERIV>
 __device__ __forceinline__ void table_lookup(const float *__restrict__ tab, int num_knots, float tx,
                                              int cb, float (&f)[3][CPL], float (&df)[3][CPL])
 {
     int kn = (int)tx;
     kn = kn > num_knots - 2 ? num_knots - 2 : kn;
-    const Hermite h = hermite_weights(tx - (float)kn);
-    const float *row0 = tab + (size_t)kn * (6 * C) + cb;
-    const float *row1 = row0 + 6 * C;
+    const float t = tx - (float)kn;
+    const float *row = tab + (size_t)kn * (12 * C) + cb;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        float f0[CPL], m0[CPL], f1[CPL], m1[CPL];
-        ldv<CPL>(row0 + k * C, f0);
-        ldv<CPL>(row0 + (3 + k) * C, m0);
-        ldv<CPL>(row1 + k * C, f1);
-        ldv<CPL>(row1 + (3 + k) * C, m1);
+        float c0[CPL], c1[CPL], c2[CPL], c3[CPL];
+        ldv<CPL>(row + k * C, c0);
+        ldv<CPL>(row + (3 + k) * C, c1);
+        ldv<CPL>(row + (6 + k) * C, c2);
+        ldv<CPL>(row + (9 + k) * C, c3);
 #pragma unroll
         for (int v = 0; v < CPL; ++v) {
-            f[k][v] = h.h00 * f0[v] + h.h10 * m0[v] + h.h01 * f1[v] + h.h11 * m1[v];
-            if (DERIV) df[k][v] = h.d00 * f0[v] + h.d10 * m0[v] + h.d01 * f1[v] + h.d11 * m1[v];
+            f[k][v] = fmaf(fmaf(fmaf(c3[v], t, c2[v]), t, c1[v]), t, c0[v]);
+            if (DERIV) df[k][v] = fmaf(fmaf(3.0f * c3[v], t, 2.0f * c2[v]), t, c1[v]);
         }
+    }
+}
+
+// one of the three radial functions (group k) at an already-split knot coordinate (kn, t)
+template <int C, int CPL>
+__device__ __forceinline__ void table_lookup_group(const float *__restrict__ tab, int kn, float t,
+                                                   int cb, int k, float (&f)[CPL], float (&df)[CPL])
+{
+    const float *row = tab + (size_t)kn * (12 * C) + cb + k * C;
+    float c0[CPL], c1[CPL], c2[CPL], c3[CPL];
+    ldv<CPL>(row, c0);
+    ldv<CPL>(row + 3 * C, c1);
+    ldv<CPL>(row + 6 * C, c2);
+    ldv<CPL>(row + 9 * C, c3);
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        f[v] = fmaf(fmaf(fmaf(c3[v], t, c2[v]), t, c1[v]), t, c0[v]);
+        df[v] = fmaf(fmaf(3.0f * c3[v], t, 2.0f * c2[v]), t, c1[v]);
     }
 }
 
@@ -291,8 +311,11 @@ __global__ void k_node_product(const float *__restrict__ Mc, const float *__rest
     st9(Qc + off, C, q);
 }
 
+// X_new = Xh + D + D*D, written either as X_new (last layer, read by the head) or directly as the
+// next layer's normalised input Xh' = X_new / (|X_new|^2 + 1) together with that norm.
 __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict__ Dc,
-                           float *__restrict__ Xn, int n, int C)
+                           float *__restrict__ Xn, float *__restrict__ Xh_next,
+                           float *__restrict__ nx_next, int n, int C)
 {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
@@ -302,7 +325,13 @@ __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict
     ld9(Xh + off, C, xh);
     ld9(Dc + off, C, dc);
     residual_fwd(xh, dc, xn);
-    st9(Xn + off, C, xn);
+    if (Xh_next) {
+        float nh[9];
+        nx_next[idx] = normalize_fwd(xn, nh);
+        st9(Xh_next + off, C, nh);
+    } else {
+        st9(Xn + off, C, xn);
+    }
 }
 
 __global__ void k_residual_bwd(const float *__restrict__ G, const float *__restrict__ Dc,
@@ -385,7 +414,7 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
     const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
     const int cb = part * 32 * CPL + lane * CPL;
-    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * (d.m.num_knots - 1) * 12 * C;
     const float *Y = d.Yc[layer];
     float acc[9][CPL];
 #pragma unroll
@@ -393,6 +422,7 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
 #pragma unroll
         for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+#pragma unroll 2
     for (int e = e0; e < e1; ++e) {
         const int j = d.col[e];
         const float4 ga = d.geoA[e];
@@ -435,8 +465,12 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
 
 // Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
 // is a gather over a's own row):
-//   G_Y[a] += sum_e f_e[:,grp] * G_M[b]              (b = sender of e)
-//   g_d[e] += sum_c sum_k <G_M[a], Yc[b]>_k * d f_e[c,k] / dd
+//   G_Y[a] += sum_e f_e[:,grp] * G_M[b]                         (b = sender of e)
+//   slot e of g_d += sum_c sum_k <G_M[b], Yc[a]>_k * d f_e[c,k]/dd
+// The second line is dE/dd of the REVERSE edge (a sends to b): the force kernel only ever uses
+// g_d[e] + g_d[reverse(e)], which is symmetric, so storing the reverse edge's term in slot e is
+// equivalent and needs no second gather (G_M[b] is already in registers, Yc[a] is the own node).
+// Two edges are processed per iteration (loads of both in flight, one shared warp reduction).
 template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
                                                           float *GY)
@@ -448,57 +482,114 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
     const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
     const int cb = part * 32 * CPL + lane * CPL;
-    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
-    const float *Y = d.Yc[layer];
-    float gma[9][CPL], acc[9][CPL];
+    const float *tab = d.m.tables + (size_t)(layer + 1) * (d.m.num_knots - 1) * 12 * C;
+    float yown[9][CPL], acc[9][CPL];
     {
-        const float *p = GM + (size_t)s * 9 * C + cb;
+        const float *p = d.Yc[layer] + (size_t)s * 9 * C + cb;
         const float *py = GY + (size_t)s * 9 * C + cb;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-            ldv<CPL>(p + q * C, gma[q]);
+            ldv<CPL>(p + q * C, yown[q]);
             ldv<CPL>(py + q * C, acc[q]);
         }
     }
     const float inv_step = 1.0f / d.m.u_step;
+    float *gd_slot = d.g_d + (size_t)part * d.capacity;
+    const int nk = d.m.num_knots;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
-    for (int e = e0; e < e1; ++e) {
-        const int j = d.col[e];
-        const float4 ga = d.geoA[e];
-        const float u = d.geoB[e].w;
-        float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, true>(tab, d.m.num_knots, ga.x, cb, f, df);
-        const float *gj = GM + (size_t)j * 9 * C + cb;
-        const float *yj = Y + (size_t)j * 9 * C + cb;
-        float gf[3][CPL];
+    for (int e = e0; e < e1; e += 2) {
+        const bool two = e + 1 < e1;
+        const int eb = two ? e + 1 : e;
+        const int j0 = d.col[e], j1 = d.col[eb];
+        float4 ga0 = d.geoA[e], ga1 = d.geoA[eb];
+        const float u0 = d.geoB[e].w, u1 = d.geoB[eb].w;
+        if (!two) ga1.y = ga1.z = 0.0f;          // the duplicated tail edge contributes nothing
+        int kn0 = (int)ga0.x, kn1 = (int)ga1.x;
+        kn0 = kn0 > nk - 2 ? nk - 2 : kn0;
+        kn1 = kn1 > nk - 2 ? nk - 2 : kn1;
+        const float t0 = ga0.x - (float)kn0, t1 = ga1.x - (float)kn1;
+        const float su0 = -u0 * inv_step * ga0.y, su1 = -u1 * inv_step * ga1.y;
+        const float *g0 = GM + (size_t)j0 * 9 * C + cb;
+        const float *g1 = GM + (size_t)j1 * 9 * C + cb;
+        float p0 = 0.0f, p1 = 0.0f;
+        // the three component groups in turn, so only one group's radial values and one or two
+        // gathered components are live at a time (registers -> occupancy)
+        {   // I: component 0, metric 3
+            float f0[CPL], df0[CPL], f1[CPL], df1[CPL], a[CPL], b[CPL];
+            table_lookup_group<C, CPL>(tab, kn0, t0, cb, 0, f0, df0);
+            table_lookup_group<C, CPL>(tab, kn1, t1, cb, 0, f1, df1);
+            ldv<CPL>(g0, a);
+            ldv<CPL>(g1, b);
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int v = 0; v < CPL; ++v) gf[k][v] = 0.0f;
-        float gmj[9][CPL], yv[9][CPL];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            ldv<CPL>(gj + q * C, gmj[q]);
-            ldv<CPL>(yj + q * C, yv[q]);
-        }
-        float psum = 0.0f;
-#pragma unroll
-        for (int v = 0; v < CPL; ++v) {
-            float a9[9], y9[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) {
-                acc[q][v] += (f[group_of(q)][v] * ga.y) * gmj[q][v];
-                a9[q] = gma[q][v];
-                y9[q] = yv[q][v];
+            for (int v = 0; v < CPL; ++v) {
+                acc[0][v] += (f0[v] * ga0.y) * a[v] + (f1[v] * ga1.y) * b[v];
+                const float y3 = 3.0f * yown[0][v];
+                p0 += a[v] * y3 * (df0[v] * su0 + f0[v] * ga0.z);
+                p1 += b[v] * y3 * (df1[v] * su1 + f1[v] * ga1.z);
             }
-            const float gI = c9_dot_I(a9, y9), gA = c9_dot_A(a9, y9), gS = c9_dot_S(a9, y9);
-            // d f_e/dd = phi * d f~/dd + f~ * dphi ;  d f~/dd = -u * (d f~/dt) / u_step
-            const float su = -u * inv_step * ga.y;
-            psum += gI * (df[0][v] * su + f[0][v] * ga.z) + gA * (df[1][v] * su + f[1][v] * ga.z) +
-                    gS * (df[2][v] * su + f[2][v] * ga.z);
         }
-        psum = nnp_warp_sum(psum);
-        if (lane == 0 && j != s) d.g_d[(size_t)part * d.capacity + e] += psum;
+        {   // A: components 1..3, metric 2
+            float f0[CPL], df0[CPL], f1[CPL], df1[CPL];
+            table_lookup_group<C, CPL>(tab, kn0, t0, cb, 1, f0, df0);
+            table_lookup_group<C, CPL>(tab, kn1, t1, cb, 1, f1, df1);
+            float da[CPL], db[CPL];
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) da[v] = db[v] = 0.0f;
+#pragma unroll
+            for (int q = 1; q < 4; ++q) {
+                float a[CPL], b[CPL];
+                ldv<CPL>(g0 + q * C, a);
+                ldv<CPL>(g1 + q * C, b);
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) {
+                    acc[q][v] += (f0[v] * ga0.y) * a[v] + (f1[v] * ga1.y) * b[v];
+                    da[v] += a[v] * yown[q][v];
+                    db[v] += b[v] * yown[q][v];
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) {
+                p0 += 2.0f * da[v] * (df0[v] * su0 + f0[v] * ga0.z);
+                p1 += 2.0f * db[v] * (df1[v] * su1 + f1[v] * ga1.z);
+            }
+        }
+        {   // S: components 4..8; <a,y>_S = a4 y4 + a5 y5 + (a4+a5)(y4+y5) + 2 (a6 y6 + a7 y7 + a8 y8)
+            float f0[CPL], df0[CPL], f1[CPL], df1[CPL];
+            table_lookup_group<C, CPL>(tab, kn0, t0, cb, 2, f0, df0);
+            table_lookup_group<C, CPL>(tab, kn1, t1, cb, 2, f1, df1);
+            float da[CPL], db[CPL];
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) da[v] = db[v] = 0.0f;
+#pragma unroll
+            for (int q = 4; q < 9; ++q) {
+                float a[CPL], b[CPL];
+                ldv<CPL>(g0 + q * C, a);
+                ldv<CPL>(g1 + q * C, b);
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) {
+                    acc[q][v] += (f0[v] * ga0.y) * a[v] + (f1[v] * ga1.y) * b[v];
+                    // weights of component q in the S inner product against the own node's Y
+                    const float wy = q == 4 ? 2.0f * yown[4][v] + yown[5][v]
+                                   : q == 5 ? 2.0f * yown[5][v] + yown[4][v]
+                                            : 2.0f * yown[q][v];
+                    da[v] += a[v] * wy;
+                    db[v] += b[v] * wy;
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) {
+                p0 += da[v] * (df0[v] * su0 + f0[v] * ga0.z);
+                p1 += db[v] * (df1[v] * su1 + f1[v] * ga1.z);
+            }
+        }
+        // one butterfly for both edges: lanes 0-15 end with the sum of p0, lanes 16-31 with p1
+        float x = (lane & 16) ? p1 : p0;
+        const float y = (lane & 16) ? p0 : p1;
+        x += __shfl_xor_sync(NNP_FULL_MASK, y, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(NNP_FULL_MASK, x, o);
+        if (lane == 0 && j0 != s) gd_slot[e] += x;
+        if (lane == 16 && two && j1 != s) gd_slot[e + 1] += x;
     }
     float *out = GY + (size_t)s * 9 * C + cb;
 #pragma unroll
@@ -875,12 +966,14 @@ int validate_model(const nnp_tn_model *m)
     return NNP_OK;
 }
 
-GemmArgs plain_gemm(const float *A, const float *W, const float *bias, float *out, int M, int N,
-                    int K, const float *aux = nullptr, int ldaux = 0)
+GemmArgs plain_gemm(const float *A, const nnp_gemm_weight &W, const float *bias, float *out, int M,
+                    int N, int K, const float *aux = nullptr, int ldaux = 0)
 {
     GemmArgs g{};
     g.A = A;
-    g.W = W;
+    g.W = W.w;
+    g.Whi = W.hi;
+    g.Wlo = W.lo;
     g.bias = bias;
     g.out = out;
     g.aux = aux;
@@ -894,15 +987,17 @@ GemmArgs plain_gemm(const float *A, const float *W, const float *bias, float *ou
 }
 
 // the three component groups (I: 1 comp, A: 3, S: 5) of a [N,9,C] tensor against W[3][C][C]
-GemmBatch mix_gemm(const float *A, const float *W3, float *out, int n, int C, float *out2 = nullptr,
-                   const float *aux = nullptr, int ldaux = 0)
+GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n, int C,
+                   float *out2 = nullptr, const float *aux = nullptr, int ldaux = 0)
 {
     static const int ncomp[3] = {1, 3, 5}, q0[3] = {0, 1, 4};
     GemmBatch b{};
     for (int k = 0; k < 3; ++k) {
         GemmArgs &g = b.g[k];
         g.A = A;
-        g.W = W3 + (size_t)k * C * C;
+        g.W = W3[k].w;
+        g.Whi = W3[k].hi;
+        g.Wlo = W3[k].lo;
         g.out = out;
         g.out2 = out2;
         g.aux = aux;
@@ -923,7 +1018,7 @@ GemmBatch mix_gemm(const float *A, const float *W3, float *out, int n, int C, fl
 // node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
 // through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
 struct EdgeTuning {
-    int emb, fwd, bwd, embbwd;
+    int emb, fwd, bwd, embbwd, bwd_block;
 };
 static int env_int(const char *name, int fallback)
 {
@@ -933,7 +1028,8 @@ static int env_int(const char *name, int fallback)
 static const EdgeTuning &edge_tuning()
 {
     static const EdgeTuning t = {env_int("NNP_CPL_EMB", 2), env_int("NNP_CPL_FWD", 4),
-                                 env_int("NNP_CPL_BWD", 2), env_int("NNP_CPL_EMBBWD", 4)};
+                                 env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
+                                 env_int("NNP_BWD_BLOCK", 128)};
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -993,13 +1089,13 @@ int run_step(TnDev &d, cudaStream_t st)
 
     // ---- interaction layers
     for (int l = 0; l < L; ++l) {
-        { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
+        if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
         { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, l))); }
-        GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + (size_t)3 * C * C, d.Dc[l], n, C);
+        GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + 3, d.Dc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
-        { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, n, C); }
+        { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, l + 1 < L ? d.Xh[l + 1] : nullptr, l + 1 < L ? d.nx[l + 1] : nullptr, n, C); }
         std::swap(X, Xother);
     }
 
@@ -1034,11 +1130,11 @@ int run_step(TnDev &d, cudaStream_t st)
     for (int l = L - 1; l >= 0; --l) {
         // GX = dL/dX_{l+1}.  dL/dXh starts as GX itself.
         { NNP_PROF("k_residual_bwd", st); k_residual_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Dc[l], Ga, n, C); }  // Ga = G_D
-        GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + (size_t)3 * C * C, Gb, n, C);     // Gb = G_Q
+        GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + 3, Gb, n, C);     // Gb = G_Q
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, l, Ga, d.Qc))); }
+        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc))); }
         // G_Xh = GX + mix^T(G_Y)  -> written in place over GX
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GX, n, C, nullptr, GX, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st))); }
@@ -1132,15 +1228,16 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 2 ? 2 : use_mma);
+    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 3 ? 3 : use_mma);
     return NNP_OK;
 }
 
-extern "C" int nnp_test_gemm_nt(const float *A, const float *W, const float *bias, float *out,
-                                int32_t M, int32_t N, int32_t K, nnp_stream_t stream)
+extern "C" int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const float *bias,
+                                float *out, int32_t M, int32_t N, int32_t K, nnp_stream_t stream)
 {
-    NNP_CHECK_ARG(A && W && out && M >= 1 && N >= 1 && K >= 4, "bad arguments to nnp_test_gemm_nt");
+    NNP_CHECK_ARG(A && W && W->w && out && M >= 1 && N >= 1 && K >= 4,
+                  "bad arguments to nnp_test_gemm_nt");
     GemmBatch b{};
-    b.g[0] = plain_gemm(A, W, bias, out, M, N, K);
+    b.g[0] = plain_gemm(A, *W, bias, out, M, N, K);
     return gemm_launch<PRO_NONE, EPI_STORE>(b, 1, static_cast<cudaStream_t>(stream));
 }

@@ -126,10 +126,11 @@ def build_radial_tables(params: Dict[str, np.ndarray], config: TNConfig):
     depend on the edge only through d, so they are 1-D functions R -> R^{3C}; the expnorm basis
     is a set of equal-width Gaussians in u, which makes u the natural abscissa (uniform knots
     resolve every basis function equally).  Values and u-derivatives are computed in float64
-    (derivative by forward mode through the MLP) and stored for cubic Hermite interpolation:
-    ``tables[t, k, 0, j, c]`` = value of output j of channel c at knot k, ``[..., 1, j, c]`` =
-    u_step * d/du.  Returns (tables float32, u_min, u_step, max interpolation error measured at
-    the knot midpoints relative to the largest table value).
+    (derivative by forward mode through the MLP); the cubic Hermite interpolant of each knot
+    interval is stored as monomial coefficients for Horner evaluation on the device:
+    ``tables[t, k, p, j, c]`` = coefficient of x^p (x in [0, 1] across interval k) of output j of
+    channel c.  Returns (tables float32, u_min, u_step, max interpolation error measured at the
+    interval midpoints relative to the largest table value).
     """
     C, K, L, nk = config.embedding_dimension, config.num_rbf, config.num_layers, config.num_knots
     u_min = float(np.exp(config.cutoff_lower - config.cutoff_upper))
@@ -156,17 +157,62 @@ def build_radial_tables(params: Dict[str, np.ndarray], config: TNConfig):
 
     knots = u_min + u_step * np.arange(nk)
     at_knots = evaluate(knots)
-    tables = np.empty((L + 1, nk, 2, 3, C), dtype=np.float64)
+    tables = np.empty((L + 1, nk - 1, 4, 3, C), dtype=np.float64)
     for t, (f, df) in enumerate(at_knots):
-        tables[t, :, 0] = f
-        tables[t, :, 1] = df * u_step
-    # interpolation error at the midpoints (t = 1/2: h00 = h01 = 1/2, h10 = 1/8, h11 = -1/8)
+        f0, f1 = f[:-1], f[1:]
+        m0, m1 = df[:-1] * u_step, df[1:] * u_step
+        tables[t, :, 0] = f0
+        tables[t, :, 1] = m0
+        tables[t, :, 2] = 3.0 * (f1 - f0) - 2.0 * m0 - m1
+        tables[t, :, 3] = 2.0 * (f0 - f1) + m0 + m1
+    # interpolation error at the interval midpoints
     mid = evaluate(knots[:-1] + 0.5 * u_step)
     err = 0.0
     for t, (f, _) in enumerate(mid):
-        interp = 0.5 * (tables[t, :-1, 0] + tables[t, 1:, 0]) + 0.125 * (tables[t, :-1, 1] - tables[t, 1:, 1])
-        err = max(err, float(np.max(np.abs(interp - f)) / max(np.max(np.abs(tables[t, :, 0])), 1e-30)))
+        c = tables[t]
+        interp = c[:, 0] + 0.5 * c[:, 1] + 0.25 * c[:, 2] + 0.125 * c[:, 3]
+        err = max(err, float(np.max(np.abs(interp - f)) / max(np.max(np.abs(c[:, 0])), 1e-30)))
     return tables.astype(np.float32), u_min, u_step, err
+
+
+def gemm_tile_n(n_out: int) -> int:
+    """Output-tile width the tcgen05 kernel uses for a weight with ``n_out`` rows."""
+    for nt in (128, 64, 32, 16):
+        if n_out % nt == 0:
+            return nt
+    raise ValidationError(f"GEMM output width {n_out} must be a multiple of 16")
+
+
+def tf32_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> nearest TF32 value (10-bit mantissa, ties away from zero, like cvt.rna.tf32)."""
+    bits = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((bits + 0x1000) & 0xFFFFE000).astype(np.uint32).view(np.float32)
+
+
+def stage_gemm_weight(w: np.ndarray):
+    """Split W[N, K] into TF32 hi/lo parts and lay both out as the shared-memory tile images the
+    tcgen05 kernel bulk-copies: [N/NT][ceil(K/32)][NT rows][32 floats] with the eight 16-byte
+    chunks of every 128-byte row XOR-swizzled by (row % 8) (K-major SWIZZLE_128B)."""
+    w32 = np.ascontiguousarray(w, dtype=np.float32)
+    n, k = w32.shape
+    nt = gemm_tile_n(n)
+    nchunks = (k + 31) // 32
+    hi = tf32_round(w32)
+    lo = tf32_round(w32 - hi)
+    out = []
+    rows = np.arange(nt)
+    kk = np.arange(32)
+    # float index of (row r, k-in-chunk kk) inside one [NT][32] block
+    idx = ((rows[:, None] >> 3) * 256 + (rows[:, None] & 7) * 32
+           + (((kk[None, :] >> 2) ^ (rows[:, None] & 7)) << 2) + (kk[None, :] & 3))
+    for part in (hi, lo):
+        padded = np.zeros((n, nchunks * 32), dtype=np.float32)
+        padded[:, :k] = part
+        blocks = padded.reshape(n // nt, nt, nchunks, 32).transpose(0, 2, 1, 3)   # [tile][chunk][r][kk]
+        img = np.empty((n // nt, nchunks, nt * 32), dtype=np.float32)
+        img[:, :, idx.ravel()] = blocks.reshape(n // nt, nchunks, nt * 32)
+        out.append(img.ravel())
+    return w32, out[0], out[1]
 
 
 class _Plan:
@@ -223,16 +269,29 @@ class TensorNet:
         m.z_send = dev("z_send", P["emb"] @ Wb.T + P["emb2_b"])
         m.tables = dev("tables", tables)
         m.init_norm_g, m.init_norm_b = dev("ing", P["init_norm_g"]), dev("inb", P["init_norm_b"])
-        m.es0_w, m.es0_wT, m.es0_b = dev("es0_w", P["es0_w"]), dev("es0_wT", P["es0_w"].T), dev("es0_b", P["es0_b"])
-        m.es1_w, m.es1_wT, m.es1_b = dev("es1_w", P["es1_w"]), dev("es1_wT", P["es1_w"].T), dev("es1_b", P["es1_b"])
-        m.et_w = dev("et_w", P["et_w"])
-        m.et_wT = dev("et_wT", np.transpose(P["et_w"], (0, 2, 1)))
+
+        def gemm_weight(slot, name, w):
+            w32, hi, lo = stage_gemm_weight(w)
+            slot.w, slot.hi, slot.lo = dev(name, w32), dev(name + ".hi", hi), dev(name + ".lo", lo)
+
+        gemm_weight(m.es0_w, "es0_w", P["es0_w"])
+        gemm_weight(m.es0_wT, "es0_wT", P["es0_w"].T)
+        gemm_weight(m.es1_w, "es1_w", P["es1_w"])
+        gemm_weight(m.es1_wT, "es1_wT", P["es1_w"].T)
+        m.es0_b, m.es1_b = dev("es0_b", P["es0_b"]), dev("es1_b", P["es1_b"])
+        for k in range(3):
+            gemm_weight(m.et_w[k], f"et_w{k}", P["et_w"][k])
+            gemm_weight(m.et_wT[k], f"et_wT{k}", P["et_w"][k].T)
         for l in range(cfg.num_layers):
-            m.layer_t_w[l] = dev(f"t_w{l}", P[f"l{l}_t_w"])
-            m.layer_t_wT[l] = dev(f"t_wT{l}", np.transpose(P[f"l{l}_t_w"], (0, 2, 1)))
+            for k in range(6):
+                gemm_weight(m.layer_t_w[l][k], f"t_w{l}_{k}", P[f"l{l}_t_w"][k])
+                gemm_weight(m.layer_t_wT[l][k], f"t_wT{l}_{k}", P[f"l{l}_t_w"][k].T)
         m.out_norm_g, m.out_norm_b = dev("ong", P["out_norm_g"]), dev("onb", P["out_norm_b"])
-        m.lin_w, m.lin_wT, m.lin_b = dev("lin_w", P["lin_w"]), dev("lin_wT", P["lin_w"].T), dev("lin_b", P["lin_b"])
-        m.h1_w, m.h1_wT, m.h1_b = dev("h1_w", P["h1_w"]), dev("h1_wT", P["h1_w"].T), dev("h1_b", P["h1_b"])
+        gemm_weight(m.lin_w, "lin_w", P["lin_w"])
+        gemm_weight(m.lin_wT, "lin_wT", P["lin_w"].T)
+        gemm_weight(m.h1_w, "h1_w", P["h1_w"])
+        gemm_weight(m.h1_wT, "h1_wT", P["h1_w"].T)
+        m.lin_b, m.h1_b = dev("lin_b", P["lin_b"]), dev("h1_b", P["h1_b"])
         m.h2_w = dev("h2_w", P["h2_w"])
         self._model = m
         self._weights = keep

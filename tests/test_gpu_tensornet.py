@@ -49,26 +49,30 @@ def check(model, z, pos, batch, box, e_tol=E_TOL, f_tol=F_TOL):
     return e_err, f_err
 
 
-@pytest.mark.parametrize("mode", [2, 1, 0])
+@pytest.mark.parametrize("mode", [2, 3, 1, 0])
 def test_gemm_tile_engine(mode):
+    """All four inner loops (persistent tcgen05, per-tile tcgen05, mma.sync, FFMA) vs float64."""
     lib = _lib.load()
     lib.nnp_set_gemm_mode(mode)
     try:
         g = torch.Generator(device="cuda").manual_seed(0)
         for M, N, K in [(64, 64, 32), (200, 128, 128), (333, 384, 256), (70, 16, 64), (129, 96, 16),
-                        (1000, 256, 128), (5000, 128, 64), (128, 32, 384)]:
+                        (1000, 256, 128), (5000, 128, 64), (128, 32, 384), (40000, 128, 128)]:
             A = torch.randn(M, K, device="cuda", generator=g)
             W = torch.randn(N, K, device="cuda", generator=g)
             bias = torch.randn(N, device="cuda", generator=g)
             out = torch.empty(M, N, device="cuda")
-            rc = lib.nnp_test_gemm_nt(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(),
+            w32, hi, lo = P.stage_gemm_weight(W.cpu().numpy())
+            hi_t, lo_t = torch.from_numpy(hi).cuda(), torch.from_numpy(lo).cuda()
+            gw = _lib.GemmWeight(W.data_ptr(), hi_t.data_ptr(), lo_t.data_ptr())
+            rc = lib.nnp_test_gemm_nt(A.data_ptr(), ctypes.byref(gw), bias.data_ptr(), out.data_ptr(),
                                       M, N, K, torch.cuda.current_stream().cuda_stream)
             assert rc == 0
             ref = (A.double() @ W.double().T + bias.double())
             err = (out.double() - ref).abs().max().item() / ref.abs().max().item()
             assert err < 5e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
     finally:
-        lib.nnp_set_gemm_mode(2)
+        lib.nnp_set_gemm_mode(3)
 
 
 def small_open(rng, n=20):
@@ -87,7 +91,7 @@ def test_small_open_system(rng, C, L):
     check(model, *small_open(rng))
 
 
-@pytest.mark.parametrize("gemm_mode", [2, 1, 0])
+@pytest.mark.parametrize("gemm_mode", [2, 3, 1, 0])
 def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
     _lib.load().nnp_set_gemm_mode(gemm_mode)
     try:
@@ -101,7 +105,7 @@ def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
                             cutoff_upper=4.5, max_z=10, seed=6)
         check(model, z, pos, None, box)
     finally:
-        _lib.load().nnp_set_gemm_mode(2)
+        _lib.load().nnp_set_gemm_mode(3)
 
 
 def test_config_a_alanine_sized_molecule():

@@ -116,16 +116,15 @@ def test_radial_tables_reproduce_the_mlp(rl):
     cfg = P.TNConfig(embedding_dimension=32, num_layers=2, num_rbf=16, cutoff_lower=rl, cutoff_upper=4.5)
     params = P.init_params(cfg, 7)
     tables, u_min, u_step, err = P.build_radial_tables(params, cfg)
-    assert tables.shape == (3, cfg.num_knots, 2, 3, 32) and err < 1e-6
+    assert tables.shape == (3, cfg.num_knots - 1, 4, 3, 32) and err < 1e-6
     d = np.random.default_rng(0).uniform(max(rl, 0.0), 4.5, 4000)
     u = np.exp(rl - d)
     x = (u - u_min) / u_step
     k = np.clip(np.floor(x).astype(int), 0, cfg.num_knots - 2)
     t = (x - k)[:, None, None]
-    tb = tables.astype(np.float64)
-    f0, m0, f1, m1 = tb[:, k, 0], tb[:, k, 1], tb[:, k + 1, 0], tb[:, k + 1, 1]
-    val = (2*t**3-3*t**2+1)*f0 + (t**3-2*t**2+t)*m0 + (-2*t**3+3*t**2)*f1 + (t**3-t**2)*m1
-    dval = ((6*t**2-6*t)*f0 + (3*t**2-4*t+1)*m0 + (-6*t**2+6*t)*f1 + (3*t**2-2*t)*m1) / u_step * (-u)[:, None, None]
+    c = tables.astype(np.float64)[:, k]                      # [tables, edges, 4, 3, C]
+    val = ((c[:, :, 3] * t + c[:, :, 2]) * t + c[:, :, 1]) * t + c[:, :, 0]
+    dval = ((3 * c[:, :, 3] * t + 2 * c[:, :, 2]) * t + c[:, :, 1]) / u_step * (-u)[:, None, None]
     rho = O.rbf_expnorm(d, params["rbf_means"], params["rbf_betas"], rl)
     drho = O.rbf_expnorm_dd(d, params["rbf_means"], params["rbf_betas"], rl)
     for l in range(2):
