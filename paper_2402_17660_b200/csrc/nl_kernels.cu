@@ -16,6 +16,7 @@
 // Two passes over the candidates (count -> exclusive scan -> fill) give each row its final
 // offset without atomics, so the output order is deterministic and equals np.lexsort((j, i)).
 #include <algorithm>
+#include <cmath>
 
 #include "nnp_common.cuh"
 
@@ -39,8 +40,16 @@ struct Metric {
     double lo2, hi2;
 };
 
+// float copy of the metric for the prefilter; hi2p / lo2m are the window widened by the
+// prefilter's error bound (relative eps of the squared distance)
+struct MetricF {
+    float b00, b10, b11, b20, b21, b22, i00, i11, i22, hi2p, lo2m;
+};
+
 struct NlArgs {
     int n, n_samples, capacity, strategy, flags, periodic, max_cells;
+    int stage_w;      // accepted candidates kept per row between the count and the fill pass
+    MetricF mf;
     double cutoff;
     double inv_box[9];
     int host_dims[3];
@@ -49,7 +58,7 @@ struct NlArgs {
     const int *batch;
     // workspace
     int *cell_id, *cell_start, *cell_cursor, *tmp_order, *sidx, *rank_of, *sbatch, *row_count;
-    int *sample_ptr, *scratch_col, *scratch_t;
+    int *sample_ptr, *scratch_col, *scratch_t, *stage_t;
     double *spos;
     double *bounds_partial;
     GridDev *grid;
@@ -89,20 +98,19 @@ __device__ __forceinline__ double pair_delta(const Metric &m, double ax, double 
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-__global__ void k_fill_i32(int *p, int64_t n, int v)
-{
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
-}
-
+// sample_ptr[b] = first atom of sample b (batch is non-decreasing, system.py:231-235)
 __global__ void k_sample_ptr(const int *__restrict__ batch, int n, int n_samples,
-                             int *__restrict__ sample_ptr)
+                             int *__restrict__ sample_ptr, int *__restrict__ counts)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int b = batch[i];
-    if (i == 0 || batch[i - 1] != b) sample_ptr[b] = i;
-    if (i == n - 1) sample_ptr[n_samples] = n;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < 4) counts[b] = 0;
+    if (b > n_samples) return;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (batch[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    sample_ptr[b] = lo;
 }
 
 // ---- open-boundary grid: bounding box reduction (neighbors.py:116-124)
@@ -234,6 +242,7 @@ __global__ void k_cell_rank(NlArgs a)
     int s = p0 + rank;
     a.sidx[s] = i;
     a.rank_of[i] = s;
+    if (a.order) a.order[s] = (a.flags & NNP_NL_RENUMBER) ? i : s;
     a.sbatch[s] = a.batch[i];
     a.spos[3 * (size_t)s] = a.pos[3 * (size_t)i];
     a.spos[3 * (size_t)s + 1] = a.pos[3 * (size_t)i + 1];
@@ -246,6 +255,7 @@ __global__ void k_identity_order(NlArgs a)
     if (i >= a.n) return;
     a.sidx[i] = i;
     a.rank_of[i] = i;
+    if (a.order) a.order[i] = i;
     a.sbatch[i] = a.batch[i];
     a.spos[3 * (size_t)i] = a.pos[3 * (size_t)i];
     a.spos[3 * (size_t)i + 1] = a.pos[3 * (size_t)i + 1];
@@ -301,16 +311,46 @@ __device__ __forceinline__ void visit_runs(const NlArgs &a, const GridDev &g, in
     }
 }
 
+// Cheap single-precision screen of a candidate: the coordinate differences are taken in float64
+// (exact to 1 ulp whatever the magnitude of the coordinates) and everything after that runs in
+// float32 against a window widened by the error bound.  Only survivors get the exact float64
+// evaluation, which alone decides membership and produces the output values.
+__device__ __forceinline__ bool prefilter(const NlArgs &a, double ax, double ay, double az, double bx,
+                                          double by, double bz)
+{
+    float fx = (float)(ax - bx), fy = (float)(ay - by), fz = (float)(az - bz);
+    const MetricF &m = a.mf;
+    if (a.periodic) {
+        float sft = rintf(fz * m.i22);
+        fx -= sft * m.b20;
+        fy -= sft * m.b21;
+        fz -= sft * m.b22;
+        sft = rintf(fy * m.i11);
+        fx -= sft * m.b10;
+        fy -= sft * m.b11;
+        fx -= m.b00 * rintf(fx * m.i00);
+    }
+    const float d2 = fx * fx + fy * fy + fz * fz;
+    return d2 <= m.hi2p && d2 >= m.lo2m;
+}
+
 template <bool FILL, typename OutT>
 __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
 {
     __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
+    __shared__ int s_queue[NL_WARPS][64];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int s = blockIdx.x * NL_WARPS + wib;
     if (s >= a.n) return;
-    if (FILL && a.row_ptr[a.n] > a.capacity) return;  // overflow: host raises CapacityError
+    if (FILL) {
+        const int total = a.row_ptr[a.n];
+        if (s == 0 && lane == 0) a.counts[0] = total;
+        if (total > a.capacity) return;          // overflow: the host raises CapacityError
+    } else if (s == 0 && lane == 0) {
+        a.row_count[a.n] = 0;                     // so that the scan's last output is the total
+    }
 
     const bool full = a.flags & NNP_NL_FULL_LIST;
     const bool renumber = a.flags & NNP_NL_RENUMBER;
@@ -320,9 +360,13 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
     const double ax = a.spos[3 * (size_t)s], ay = a.spos[3 * (size_t)s + 1],
                  az = a.spos[3 * (size_t)s + 2];
     const Metric m = a.metric;
+    int *queue = s_queue[wib];
+    int *stage = a.stage_t + (size_t)s * a.stage_w;
 
     int *list_col = nullptr, *list_t = nullptr;
     int row_start = 0;
+    bool from_stage = false;
+    int cnt = 0;
     if (FILL) {
         row_start = a.row_ptr[row];
         const int expect = a.row_ptr[row + 1] - row_start;
@@ -333,51 +377,92 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
             list_col = a.scratch_col + row_start;
             list_t = a.scratch_t + row_start;
         }
+        if (expect <= a.stage_w) {
+            // the count pass kept this row's accepted candidates: no second scan
+            from_stage = true;
+            for (int e = lane; e < expect; e += 32) {
+                const int t = stage[e];
+                list_t[e] = t;
+                list_col[e] = renumber ? t : a.sidx[t];
+            }
+            cnt = expect;
+        }
     }
 
-    int cnt = 0;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    auto process = [&](int p0, int p1) {
-        for (int base = p0; base < p1; base += 32) {
-            const int t = base + lane;
+    if (!from_stage) {
+        const unsigned lt_mask = (1u << lane) - 1u;
+        int qn = 0;
+        // exact float64 test of up to 32 queued candidates (one per lane)
+        auto exact_step = [&](int t, bool valid) {
             bool ok = false;
             int jo = 0;
-            if (t < p1) {
+            if (valid) {
                 jo = a.sidx[t];
-                if (a.sbatch[t] == bi && jo != io && (full || jo > io)) {
-                    const double bx = a.spos[3 * (size_t)t], by = a.spos[3 * (size_t)t + 1],
-                                 bz = a.spos[3 * (size_t)t + 2];
-                    double dx, dy, dz, d2;
-                    if (io < jo)
-                        d2 = pair_delta(m, ax, ay, az, bx, by, bz, dx, dy, dz);
-                    else
-                        d2 = pair_delta(m, bx, by, bz, ax, ay, az, dx, dy, dz);
-                    ok = d2 > m.lo2 && d2 <= m.hi2;
-                }
+                const double bx = a.spos[3 * (size_t)t], by = a.spos[3 * (size_t)t + 1],
+                             bz = a.spos[3 * (size_t)t + 2];
+                double dx, dy, dz, d2;
+                if (io < jo)
+                    d2 = pair_delta(m, ax, ay, az, bx, by, bz, dx, dy, dz);
+                else
+                    d2 = pair_delta(m, bx, by, bz, ax, ay, az, dx, dy, dz);
+                ok = d2 > m.lo2 && d2 <= m.hi2;
             }
             const unsigned hit = __ballot_sync(NNP_FULL_MASK, ok);
-            if (FILL && ok) {
+            if (ok) {
                 const int p = cnt + __popc(hit & lt_mask);
-                list_col[p] = renumber ? t : jo;
-                list_t[p] = t;
+                if (FILL) {
+                    list_col[p] = renumber ? t : jo;
+                    list_t[p] = t;
+                } else if (p < a.stage_w) {
+                    stage[p] = t;
+                }
             }
             cnt += __popc(hit);
+        };
+        auto process = [&](int p0, int p1) {
+            for (int base = p0; base < p1; base += 32) {
+                const int t = base + lane;
+                bool pass = false;
+                if (t < p1) {
+                    const int jo = a.sidx[t];
+                    if (a.sbatch[t] == bi && jo != io && (full || jo > io))
+                        pass = prefilter(a, ax, ay, az, a.spos[3 * (size_t)t],
+                                         a.spos[3 * (size_t)t + 1], a.spos[3 * (size_t)t + 2]);
+                }
+                const unsigned mk = __ballot_sync(NNP_FULL_MASK, pass);
+                if (pass) queue[qn + __popc(mk & lt_mask)] = t;
+                qn += __popc(mk);
+                __syncwarp();
+                if (qn >= 32) {
+                    const int tq = queue[qn - 32 + lane];
+                    qn -= 32;
+                    exact_step(tq, true);
+                    __syncwarp();
+                }
+            }
+        };
+        GridDev g{};
+        int cell = 0;
+        if (a.strategy == NNP_STRATEGY_CELL) {
+            g = *a.grid;
+            cell = a.cell_id[io];
         }
-    };
-    GridDev g{};
-    int cell = 0;
-    if (a.strategy == NNP_STRATEGY_CELL) {
-        g = *a.grid;
-        cell = a.cell_id[io];
-    }
-    visit_runs(a, g, cell, bi, process);
-
-    if (a.flags & NNP_NL_SELF_LOOPS) {
-        if (FILL && lane == 0) {
-            list_col[cnt] = row;
-            list_t[cnt] = s;
+        visit_runs(a, g, cell, bi, process);
+        if (qn > 0) {
+            const bool valid = lane < qn;
+            exact_step(valid ? queue[lane] : 0, valid);
         }
-        cnt += 1;
+        if (a.flags & NNP_NL_SELF_LOOPS) {
+            if (lane == 0) {
+                if (FILL) {
+                    list_col[cnt] = row;
+                    list_t[cnt] = s;
+                } else if (cnt < a.stage_w) {
+                    stage[cnt] = s;
+                }
+            }
+            cnt += 1;
+        }
     }
 
     if (!FILL) {
@@ -422,11 +507,6 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
     }
 }
 
-__global__ void k_total(NlArgs a)
-{
-    if (threadIdx.x == 0 && blockIdx.x == 0) a.counts[0] = a.row_ptr[a.n];
-}
-
 template <typename OutT>
 __global__ void k_pad_tail(NlArgs a)
 {
@@ -439,12 +519,6 @@ __global__ void k_pad_tail(NlArgs a)
     OutT *dists = static_cast<OutT *>(a.dists);
     deltas[3 * idx] = deltas[3 * idx + 1] = deltas[3 * idx + 2] = (OutT)0;
     dists[idx] = (OutT)0;
-}
-
-__global__ void k_copy_order(NlArgs a)
-{
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < a.n) a.order[i] = (a.flags & NNP_NL_RENUMBER) ? a.sidx[i] : i;
 }
 
 __global__ void k_f32_to_f64(const float *__restrict__ src, double *__restrict__ dst, int64_t n)
@@ -477,6 +551,13 @@ __global__ void k_pullback(const int *__restrict__ pairs, const double *__restri
 
 constexpr int BOUNDS_BLOCKS = 128;
 
+// accepted candidates kept per row between the two passes: 1.5x the mean row the capacity allows
+int stage_width(const nnp_nl_params *p)
+{
+    int64_t w = (3 * (int64_t)p->capacity) / (2 * (int64_t)p->n_atoms) + 8;
+    return (int)std::min<int64_t>(std::max<int64_t>(w, 16), NL_MAXROW);
+}
+
 size_t carve(NlArgs &a, const nnp_nl_params *p, void *ws)
 {
     NnpArena ar(ws);
@@ -493,6 +574,8 @@ size_t carve(NlArgs &a, const nnp_nl_params *p, void *ws)
     a.sample_ptr = ar.take<int>((size_t)p->n_samples + 1);
     a.scratch_col = ar.take<int>((size_t)p->capacity);
     a.scratch_t = ar.take<int>((size_t)p->capacity);
+    a.stage_w = stage_width(p);
+    a.stage_t = ar.take<int>(n * (size_t)a.stage_w);
     a.spos = ar.take<double>(3 * n);
     a.bounds_partial = ar.take<double>(6 * BOUNDS_BLOCKS);
     a.grid = ar.take<GridDev>(1);
@@ -579,6 +662,20 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
         m.i11 = 1.0 / m.b11;
         m.i22 = 1.0 / m.b22;
     }
+    {
+        // prefilter window: relative error of the float32 squared distance.  Differences enter
+        // exact to 1 ulp(float); the periodic reduction adds ~ulp(box length) per component.
+        double span = 0.0;
+        if (a.periodic)
+            for (int k = 0; k < 9; ++k) span = std::max(span, std::fabs(p->box[k]));
+        const double eps = 32.0 * 1.1920929e-7 * (1.0 + 3.0 * span / p->cutoff_upper);
+        MetricF &f = a.mf;
+        f.b00 = (float)m.b00; f.b10 = (float)m.b10; f.b11 = (float)m.b11;
+        f.b20 = (float)m.b20; f.b21 = (float)m.b21; f.b22 = (float)m.b22;
+        f.i00 = (float)m.i00; f.i11 = (float)m.i11; f.i22 = (float)m.i22;
+        f.hi2p = (float)(m.hi2 * (1.0 + eps)) * 1.000001f;
+        f.lo2m = m.lo2 > 0.0 ? (float)(m.lo2 * (1.0 - eps)) * 0.999999f : -1.0f;
+    }
     a.pos = pos;
     a.batch = batch;
     a.pairs = pairs;
@@ -591,9 +688,7 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
 
     const int n = a.n;
     const int nb = nnp_blocks(n, 256);
-    cudaMemsetAsync(counts, 0, 4 * sizeof(int), stream);
-    { NNP_PROF("k_fill_i32", stream); k_fill_i32<<<NNP_GRID(nnp_blocks(a.n_samples + 1, 256)), 256, 0, stream>>>(a.sample_ptr, a.n_samples + 1, n); }
-    { NNP_PROF("k_sample_ptr", stream); k_sample_ptr<<<NNP_GRID(nb), 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr); }
+    { NNP_PROF("k_sample_ptr", stream); k_sample_ptr<<<NNP_GRID(nnp_blocks(a.n_samples + 1, 256)), 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr, counts); }
 
     if (a.strategy == NNP_STRATEGY_CELL) {
         int n_partial = 1;
@@ -602,8 +697,8 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
             { NNP_PROF("k_bounds_partial", stream); k_bounds_partial<<<NNP_GRID(n_partial), NL_THREADS, 0, stream>>>(pos, n, a.bounds_partial); }
         }
         { NNP_PROF("k_grid_setup", stream); k_grid_setup<<<NNP_GRID(1), 32, 0, stream>>>(a, n_partial); }
-        cudaMemsetAsync(a.cell_start, 0, ((size_t)a.max_cells + 1) * sizeof(int), stream);
-        cudaMemsetAsync(a.cell_cursor, 0, (size_t)a.max_cells * sizeof(int), stream);
+        // cell_start (max_cells + 1 ints) and cell_cursor (max_cells ints) are carved back to back
+        cudaMemsetAsync(a.cell_start, 0, (size_t)((char *)(a.cell_cursor + a.max_cells) - (char *)a.cell_start), stream);
         { NNP_PROF("k_cell_assign", stream); k_cell_assign<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
         {
             NNP_PROF("scan_cells", stream);
@@ -621,14 +716,11 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
     const int row_blocks = nnp_blocks(n, NL_WARPS);
     const bool f32 = p->flags & NNP_NL_F32_OUT;
     { NNP_PROF("k_rows_count", stream); k_rows<false, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
-    // row_count has n entries; entry n must be zero so the scan's last output is the total
-    cudaMemsetAsync(a.row_count + n, 0, sizeof(int), stream);
     {
         NNP_PROF("scan_rows", stream);
         rc = nnp_exclusive_scan_i32(a.row_count, a.row_ptr, (int64_t)n + 1, scan_temp, stream);
     }
     if (rc) return rc;
-    { NNP_PROF("k_total", stream); k_total<<<NNP_GRID(1), 32, 0, stream>>>(a); }
     if (f32)
         { NNP_PROF("k_rows_fill", stream); k_rows<true, float><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
     else
@@ -639,7 +731,6 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
         else
             { NNP_PROF("k_pad_tail", stream); k_pad_tail<double><<<NNP_GRID(nnp_blocks(a.capacity, 256)), 256, 0, stream>>>(a); }
     }
-    if (order) k_copy_order<<<NNP_GRID(nb), 256, 0, stream>>>(a);
     NNP_CHECK_LAUNCH("neighbor rows");
     return NNP_OK;
 }
