@@ -121,8 +121,8 @@ def algorithmic_bytes(n_atoms: int, n_edges: int, n_cells: int):
     T = 9 * CHANNELS * 4
     L = LAYERS
     per_kernel = {
-        "k_edge_message": 2 * T * n_atoms + 20 * n_edges,
-        "k_edge_message_bwd": 4 * T * n_atoms + 44 * n_edges,
+        "k_edge_message": 4 * T * n_atoms + 20 * n_edges,      # read Y' (gather + own), write M and Q
+        "k_edge_message_bwd": 4 * T * n_atoms + 28 * n_edges,  # read G_M, Y', G_Y; write G_Y; edges
         "k_embed_edge": T * n_atoms + 8 * CHANNELS * n_atoms + 36 * n_edges,
         "k_embed_edge_bwd": T * n_atoms + 60 * n_edges,
         "gemm_mix": 2 * T * n_atoms,

@@ -28,6 +28,7 @@ struct GemmArgs {
     int M, N, K;
     int lda, ldo, ldaux;
     int ncomp, q0, grp;  // ncomp > 0: logical row r -> physical row (r / ncomp) * 9 + q0 + r % ncomp
+    int dbg;             // measurement switches (NNP_GEMM_DBG): 1 skip loads, 2 skip MMAs, 4 skip stores
 };
 
 struct GemmBatch {
@@ -36,18 +37,40 @@ struct GemmBatch {
 
 constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 32, GEMM_LD = GEMM_BK + 4, GEMM_THREADS = 256;
 
-__device__ __forceinline__ int gemm_phys_row(const GemmArgs &g, int r)
+// logical row -> physical row of the [node][9][C] layout; the component counts are 1, 3 or 5, so the
+// division is by a compile-time constant in every real case (a runtime divide costs ~25 dependent
+// instructions and sat on the critical path of the store loop)
+__device__ __forceinline__ int phys_row_of(int ncomp, int q0, int r)
 {
-    if (g.ncomp == 0) return r;
-    const int node = r / g.ncomp;
-    return node * 9 + g.q0 + (r - node * g.ncomp);
+    switch (ncomp) {
+    case 0: return r;
+    case 1: return r * 9 + q0;
+    case 3: { const int n = r / 3; return n * 9 + q0 + (r - n * 3); }
+    case 5: { const int n = r / 5; return n * 9 + q0 + (r - n * 5); }
+    default: { const int n = r / ncomp; return n * 9 + q0 + (r - n * ncomp); }
+    }
 }
 
+__device__ __forceinline__ int node_of(int ncomp, int r)
+{
+    switch (ncomp) {
+    case 0: case 1: return r;
+    case 3: return r / 3;
+    case 5: return r / 5;
+    default: return r / ncomp;
+    }
+}
+
+__device__ __forceinline__ int gemm_phys_row(const GemmArgs &g, int r) { return phys_row_of(g.ncomp, g.q0, r); }
+
+// x = hi + lo with hi a TF32 value (10-bit mantissa, round to nearest by integer add-and-mask) and
+// lo the exact FP32 remainder (the tensor core reads its top 19 bits).  Three integer/FP
+// instructions; cvt.rna.tf32.f32 is not used because ptxas expands it into a long NaN/Inf-safe
+// sequence on sm_100a, which made the split -- not the MMAs -- the bottleneck of the GEMMs.
 __device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
 {
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-    const float rest = x - __uint_as_float(hi);
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(rest));
+    hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2])
@@ -71,7 +94,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs &g, int r, int c, f
     } else if (EPI == EPI_MUL_SILU_GRAD) {
         g.out[o] = v * nnp_silu_grad(g.aux[(size_t)pr * g.ldaux + c]);
     } else if (EPI == EPI_GATE) {
-        const int node = g.ncomp ? r / g.ncomp : r;
+        const int node = node_of(g.ncomp, r);
         g.out2[o] = v;
         g.out[o] = v * nnp_silu(g.aux[(size_t)node * g.ldaux + 3 * c + g.grp]);
     } else {
@@ -103,7 +126,7 @@ __device__ __forceinline__ void gemm_epilogue4(const GemmArgs &g, int r, int c, 
         v.w *= nnp_silu_grad(a.w);
         *reinterpret_cast<float4 *>(g.out + o) = v;
     } else if (EPI == EPI_GATE) {
-        const int node = g.ncomp ? r / g.ncomp : r;
+        const int node = node_of(g.ncomp, r);
         const float *a = g.aux + (size_t)node * g.ldaux + 3 * c + g.grp;
         *reinterpret_cast<float4 *>(g.out2 + o) = v;
         v.x *= nnp_silu(__ldg(a));
@@ -124,7 +147,7 @@ __device__ __forceinline__ void gemm_epilogue4(const GemmArgs &g, int r, int c, 
 template <int PRO, int EPI, bool MMA>
 __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
 {
-    const GemmArgs g = batch.g[blockIdx.z];
+    const GemmArgs &g = batch.g[blockIdx.z];
     const int m0 = blockIdx.x * GEMM_BM;
     const int n0 = blockIdx.y * GEMM_BN;
     if (m0 >= g.M || n0 >= g.N) return;

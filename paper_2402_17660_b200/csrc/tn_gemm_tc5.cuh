@@ -18,6 +18,8 @@
 // 32*w + t.
 #pragma once
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "tn_gemm.cuh"
@@ -131,13 +133,13 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     constexpr int TMEM_COLS = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
     constexpr int A_PASSES = BM / 16;   // 128 threads cover 16 rows x 8 chunks per pass
     constexpr int W_PASSES = NT / 16;
-    const GemmArgs g = batch.g[blockIdx.z];
+    const GemmArgs &g = batch.g[blockIdx.z];
     const int m0 = blockIdx.x * BM;
     const int n0 = blockIdx.y * NT;
     if (m0 >= g.M || n0 >= g.N) return;
 
     extern __shared__ char smem_raw[];
-    char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space
     char *a_hi = smem, *a_lo = smem + BM * 128;
     char *w_hi = smem + 2 * BM * 128, *w_lo = w_hi + NT * 128;
     __shared__ uint64_t mma_bar;
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     __syncthreads();
     // phase 2: one warp per row, one float4 per lane -> coalesced global stores
     constexpr int ROWS_PER_IT = 32 / CH;          // rows a warp covers per iteration (NT < 128)
+#pragma unroll 4
     for (int it = warp * ROWS_PER_IT; it < BM; it += 4 * ROWS_PER_IT) {
         const int rr = it + lane / CH;
         const int ch = lane % CH;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_tc5_ws_kernel(GemmBatch ba
     constexpr int CH = NT / 4;
 
     extern __shared__ char smem_raw[];
-    char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space
     float *stage_out = reinterpret_cast<float *>(smem + WS_STAGES * STAGE_BYTES);
     __shared__ uint64_t full_bar[WS_STAGES], empty_bar[WS_STAGES], tfull_bar[2], tempty_bar[2];
     __shared__ uint32_t tmem_base_s;
@@ -545,6 +548,293 @@ static int launch_ws(const GemmBatch &b, int count, cudaStream_t stream)
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Weight-stationary kernel for the channel-mixing GEMMs (N = K = 128): the model's hot GEMM shape.
+//
+//   out^T[n, r] = sum_k W[n, k] * X[r, k]
+//
+// The roles of the operands are swapped with respect to the kernels above: the 128 x 128 weight
+// matrix is the MMA's A operand and lives in TENSOR MEMORY for the whole life of the CTA (TF32
+// hi part in columns [0,128), lo part in [128,256); lane = output channel), written once with
+// tcgen05.st.  The activation rows stream through shared memory as the B operand (K-major
+// SWIZZLE_128B, hi/lo split on the fly by 8 producer warps, 4 stages deep, loads issued two
+// chunks ahead), and two 128-column accumulators ([256,384) and [384,512)) let the epilogue of one
+// row tile overlap the MMAs of the next.  With the weights out of shared memory the whole 227 KB
+// goes to activation staging, which is what it takes to keep enough HBM requests in flight.
+// CTAs are persistent and bound to one component group (one weight matrix); the three groups get
+// CTAs in proportion to their row counts.
+constexpr int WST_STAGES = 4;
+constexpr int WST_PRODUCERS = 256;
+constexpr int WST_THREADS = 128 + WST_PRODUCERS + 32;
+constexpr int WST_STAGE_BYTES = 2 * BM * 128;   // 128 rows x 128 B, hi and lo
+
+__device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+struct WstatSchedule {
+    int cta_begin[4];   // CTAs [cta_begin[z], cta_begin[z+1]) serve problem z
+};
+
+template <int PRO, int EPI>
+__global__ void __launch_bounds__(WST_THREADS, 1) gemm_wstat_kernel(GemmBatch batch, WstatSchedule sched)
+{
+    constexpr int N = 128, K = 128, NCHUNK = K / KC;
+    extern __shared__ char smem_raw[];
+    char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space
+    float *stage_out = reinterpret_cast<float *>(smem + WST_STAGES * WST_STAGE_BYTES);
+    __shared__ uint64_t full_bar[WST_STAGES], empty_bar[WST_STAGES], tfull_bar[2], tempty_bar[2];
+    __shared__ uint32_t tmem_base_s;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int z = 0;
+    while (z < 2 && (int)blockIdx.x >= sched.cta_begin[z + 1]) ++z;
+    const int my = blockIdx.x - sched.cta_begin[z];
+    const int stride = sched.cta_begin[z + 1] - sched.cta_begin[z];
+    const GemmArgs &g = batch.g[z];
+    const int tiles = (g.M + BM - 1) / BM;
+
+    if (tid == 0) {
+        for (int s = 0; s < WST_STAGES; ++s) {
+            mbar_init(&full_bar[s], WST_PRODUCERS);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull_bar[a], 1);
+            mbar_init(&tempty_bar[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = tmem_base_s;
+
+    // weights -> tensor memory (once): lane = output channel n, column k (hi) / 128 + k (lo)
+    if (warp < 4) {
+        const int n = warp * 32 + lane;
+        const float *wrow = g.W + (size_t)n * K;
+        const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+        for (int k0 = 0; k0 < K; k0 += 16) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(wrow + k0 + 4 * q));
+                tf32_split(v.x, hi[4 * q], lo[4 * q]);
+                tf32_split(v.y, hi[4 * q + 1], lo[4 * q + 1]);
+                tf32_split(v.z, hi[4 * q + 2], lo[4 * q + 2]);
+                tf32_split(v.w, hi[4 * q + 3], lo[4 * q + 3]);
+            }
+            tmem_st16(lane_addr + (uint32_t)k0, hi);
+            tmem_st16(lane_addr + (uint32_t)(K + k0), lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    if (warp >= 4 && warp < 12) {
+        // ============================================================ producers (256 threads)
+        const int ptid = tid - 128;
+        const int lrow = ptid >> 3, lchunk = ptid & 7;      // 32 rows x 8 chunks per pass, 4 passes
+        constexpr int PASSES = BM / 32;
+        const int total = ((tiles - my + stride - 1) / stride) * NCHUNK;   // chunks this CTA produces
+        float4 buf[2][PASSES];
+        auto issue = [&](int it, float4 (&dst)[PASSES]) {
+            const int tile = my + (it / NCHUNK) * stride;
+            const int k0 = (it % NCHUNK) * KC + lchunk * 4;
+#pragma unroll
+            for (int p = 0; p < PASSES; ++p) {
+                const int r = tile * BM + p * 32 + lrow;
+                dst[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < g.M && !(g.dbg & 1))
+                    dst[p] = __ldg(reinterpret_cast<const float4 *>(g.A + (size_t)gemm_phys_row(g, r) * g.lda + k0));
+            }
+        };
+        auto produce = [&](int it, float4 (&cur)[PASSES]) {
+            const int s = it % WST_STAGES;
+            const uint32_t ph = (uint32_t)((it / WST_STAGES) & 1);
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            char *x_hi = smem + s * WST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
+            if (!(g.dbg & 32)) {
+#pragma unroll
+                for (int p = 0; p < PASSES; ++p) {
+                    float4 v = cur[p];
+                    if (PRO == PRO_SILU) {
+                        v.x = nnp_silu(v.x);
+                        v.y = nnp_silu(v.y);
+                        v.z = nnp_silu(v.z);
+                        v.w = nnp_silu(v.w);
+                    }
+                    split_store(x_hi, x_lo, swz(p * 32 + lrow, lchunk), v);
+                }
+            }
+            if (!(g.dbg & 8)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&full_bar[s]);
+            if (it + 2 < total) issue(it + 2, cur);             // two chunks ahead
+        };
+        if (total > 0) issue(0, buf[0]);
+        if (total > 1) issue(1, buf[1]);
+        for (int it = 0; it < total; it += 2) {                 // ping-pong with static buffers
+            produce(it, buf[0]);
+            if (it + 1 < total) produce(it + 1, buf[1]);
+        }
+    } else if (warp == 12) {
+        // ================================================================ MMA issue (1 thread)
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(N);
+            int it = 0, tcount = 0;
+            for (int tile = my; tile < tiles; tile += stride, ++tcount) {
+                const int acc = tcount & 1;
+                const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+                mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t tmem_d = tmem_base + (uint32_t)(2 * K + acc * N);
+                for (int c = 0; c < NCHUNK; ++c, ++it) {
+                    const int s = it % WST_STAGES;
+                    const uint32_t ph = (uint32_t)((it / WST_STAGES) & 1);
+                    char *x_hi = smem + s * WST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
+                    mbar_wait(&full_bar[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t dx_hi = make_desc(smem_u32(x_hi)), dx_lo = make_desc(smem_u32(x_lo));
+#pragma unroll
+                    for (int ks = 0; ks < KC / 8; ++ks) {
+                        if (g.dbg & 2) break;
+                        const uint64_t adv = (uint64_t)(ks * 32 >> 4);
+                        const uint32_t kcol = (uint32_t)(c * KC + ks * 8);
+                        umma_tf32_ta(tmem_d, tmem_base + K + kcol, dx_hi + adv, idesc, (c | ks) != 0);  // W_lo * X_hi
+                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_lo + adv, idesc, 1);                  // W_hi * X_lo
+                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_hi + adv, idesc, 1);                  // W_hi * X_hi
+                    }
+                    umma_commit(&empty_bar[s]);
+                    if (c + 1 == NCHUNK) umma_commit(&tfull_bar[acc]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < 4) {
+        // ==================================================================== epilogue
+        int tcount = 0;
+        const int n = warp * 32 + lane;                     // this thread's accumulator lane = channel
+        for (int tile = my; tile < tiles; tile += stride, ++tcount) {
+            const int acc = tcount & 1;
+            const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+            mbar_wait(&tfull_bar[acc], acc_ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 16) {
+                if (g.dbg & 16) break;
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(2 * K + acc * N + c0), v);
+                // v[i] = out[row c0 + i][channel n]: transpose through the [row][channel] staging tile
+#pragma unroll
+                for (int i = 0; i < 16; ++i) stage_out[(c0 + i) * N + n] = v[i];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty_bar[acc]);
+            if (EPI == EPI_STORE && g.bias == nullptr && !(g.dbg & 512)) {
+                // plain store: hand the staged rows to the bulk-copy engine (one 512-byte
+                // cp.async.bulk per output row, issued by one lane per warp), no per-lane traffic
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (lane == 0) {
+                    for (int row = warp; row < BM; row += 4) {
+                        const int r = tile * BM + row;
+                        if (r < g.M) {
+                            float *dst = g.out + (size_t)gemm_phys_row(g, r) * g.ldo;
+                            asm volatile(
+                                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                                "r"(smem_u32(stage_out + row * N)), "r"(N * 4)
+                                : "memory");
+                        }
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging readable again
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            } else {
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll 4
+                for (int row = warp; row < BM; row += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(stage_out + row * N + lane * 4);
+                    if (!(g.dbg & 4)) gemm_epilogue4<EPI>(g, tile * BM + row, lane * 4, v);
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512)
+                     : "memory");
+    }
+}
+
+template <int PRO, int EPI>
+static int launch_wstat(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    if (count < 1 || count > 3) return -100;
+    for (int i = 0; i < count; ++i)
+        if (b.g[i].N != 128 || b.g[i].K != 128 || b.g[i].lda % 4 != 0) return -100;
+    constexpr int smem = WST_STAGES * WST_STAGE_BYTES + BM * 128 * 4 + 1024;
+    static int num_sms = 0;
+    if (num_sms == 0) {
+        cudaFuncSetAttribute(gemm_wstat_kernel<PRO, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    // CTAs per problem in proportion to its tiles (at least one, at most one per tile)
+    int tiles[3] = {0, 0, 0}, total = 0;
+    for (int i = 0; i < count; ++i) {
+        tiles[i] = (b.g[i].M + BM - 1) / BM;
+        total += tiles[i];
+    }
+    if (total <= 0) return NNP_OK;
+    WstatSchedule sc{};
+    int used = 0;
+    for (int i = 0; i < count; ++i) {
+        int c = (int)(((int64_t)tiles[i] * num_sms + total - 1) / total);
+        c = std::max(1, std::min(c, tiles[i]));
+        if (tiles[i] == 0) c = 0;
+        sc.cta_begin[i] = used;
+        used += c;
+    }
+    for (int i = count; i < 4; ++i) sc.cta_begin[i] = used;
+    gemm_wstat_kernel<PRO, EPI><<<NNP_GRID(used), WST_THREADS, smem, stream>>>(b, sc);
+    NNP_CHECK_LAUNCH("gemm_wstat");
+    return NNP_OK;
+}
+
 template <int PRO, int EPI, int NT>
 static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStream_t stream)
 {
@@ -584,8 +874,13 @@ static int launch(const GemmBatch &b, int count, cudaStream_t stream)
 }  // namespace tc5
 
 template <int PRO, int EPI>
-static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
+static int gemm_launch(const GemmBatch &b_in, int count, cudaStream_t stream)
 {
+    GemmBatch b = b_in;
+    {
+        static const int dbg = getenv("NNP_GEMM_DBG") ? atoi(getenv("NNP_GEMM_DBG")) : 0;
+        for (int i = 0; i < count; ++i) b.g[i].dbg = dbg;
+    }
     int maxM = 0, maxN = 0;
     for (int i = 0; i < count; ++i) {
         maxM = b.g[i].M > maxM ? b.g[i].M : maxM;
@@ -597,7 +892,9 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
     }
     if (maxM <= 0) return NNP_OK;
     if (g_nnp_gemm_use_mma >= 2) {
-        int rc = g_nnp_gemm_use_mma == 2 ? tc5::launch_ws<PRO, EPI>(b, count, stream) : -100;
+        int rc = -100;
+        if (g_nnp_gemm_use_mma == 4) rc = tc5::launch_wstat<PRO, EPI>(b, count, stream);
+        if (g_nnp_gemm_use_mma == 2) rc = tc5::launch_ws<PRO, EPI>(b, count, stream);
         if (rc == -100) rc = tc5::launch<PRO, EPI>(b, count, stream);
         if (rc != -100) return rc;
     }

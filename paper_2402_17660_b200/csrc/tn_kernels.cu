@@ -1228,7 +1228,7 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 3 ? 3 : use_mma);
+    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 4 ? 4 : use_mma);
     return NNP_OK;
 }
 

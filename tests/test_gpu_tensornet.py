@@ -49,9 +49,10 @@ def check(model, z, pos, batch, box, e_tol=E_TOL, f_tol=F_TOL):
     return e_err, f_err
 
 
-@pytest.mark.parametrize("mode", [2, 3, 1, 0])
+@pytest.mark.parametrize("mode", [4, 2, 3, 1, 0])
 def test_gemm_tile_engine(mode):
-    """All four inner loops (persistent tcgen05, per-tile tcgen05, mma.sync, FFMA) vs float64."""
+    """All inner loops (weight-stationary tcgen05 with W in TMEM, persistent tcgen05, per-tile tcgen05,
+    mma.sync, FFMA) against float64."""
     lib = _lib.load()
     lib.nnp_set_gemm_mode(mode)
     try:
@@ -91,7 +92,7 @@ def test_small_open_system(rng, C, L):
     check(model, *small_open(rng))
 
 
-@pytest.mark.parametrize("gemm_mode", [2, 3, 1, 0])
+@pytest.mark.parametrize("gemm_mode", [4, 2, 3, 1, 0])
 def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
     _lib.load().nnp_set_gemm_mode(gemm_mode)
     try:
