@@ -134,10 +134,15 @@ typedef struct nnp_tn_model {
     /* species tables: Z_e = z_recv[z_i] + z_send[z_j]  (emb2 bias folded into z_send) */
     const float *z_recv; /* [max_z, C] */
     const float *z_send; /* [max_z, C] */
-    /* radial tables [(L+1)][num_knots-1][4][3][C]: table 0 = distance projections dp1..3 of the
-       embedding, table 1+l = radial MLP of layer l (before the cosine envelope); per knot interval
-       the monomial coefficients c0..c3 of the cubic Hermite interpolant in x = (u-u_k)/u_step */
+    /* radial tables [(L+1)][num_knots][2][3][C]: table 0 = distance projections dp1..3 of the
+       embedding, table 1+l = radial MLP of layer l (before the cosine envelope); per knot the
+       values and the slopes (times u_step) that define the cubic Hermite interpolant in
+       x = (u-u_k)/u_step on each knot interval */
     const float *tables;
+    /* the same interpolants expanded per knot interval into monomial coefficients c0..c3 of
+       x = (u-u_k)/u_step: [(L+1)][num_knots-1][4][3][C] (Horner form for the kernels that visit
+       intervals in no particular order) */
+    const float *tables_mono;
     const float *init_norm_g, *init_norm_b;             /* [C] */
     nnp_gemm_weight es0_w, es0_wT;                      /* [2C,C], [C,2C] */
     nnp_gemm_weight es1_w, es1_wT;                      /* [3C,2C], [2C,3C] */

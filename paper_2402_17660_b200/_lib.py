@@ -54,7 +54,7 @@ class TnModel(ctypes.Structure):
         ("num_knots", _i32),
         ("cutoff_lower", _f), ("cutoff_upper", _f), ("u_min", _f), ("u_step", _f),
         ("mean", _f), ("std", _f), ("h2_b", _f),
-        ("z_recv", _p), ("z_send", _p), ("tables", _p),
+        ("z_recv", _p), ("z_send", _p), ("tables", _p), ("tables_mono", _p),
         ("init_norm_g", _p), ("init_norm_b", _p),
         ("es0_w", GemmWeight), ("es0_wT", GemmWeight),
         ("es1_w", GemmWeight), ("es1_wT", GemmWeight),

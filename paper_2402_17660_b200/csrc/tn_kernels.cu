@@ -64,14 +64,16 @@ constexpr int NNP_PARTS = 4;  // max channel parts a node's row is split over (C
 struct TnDev {
     nnp_tn_model m;
     int n, n_samples, capacity;
+    int dbg_nosort;  // measurement only: keep the caller's (sender-sorted) order inside rows
+    int dbg_col;  // measurement only: gather the own row instead of the sender's
     int nparts;  // channel-part slots of g_d / g_u in use this step (<= NNP_PARTS)
     // inputs
     const int *species, *batch, *order, *row_ptr, *pairs, *nl_counts;
     const float *deltas, *dists;
     // outputs
     float *energy, *forces, *per_atom;
-    // workspace: edges
-    int *col;
+    // workspace: edges (model order: CSR by receiver, each row sorted by table coordinate)
+    int *col, *rev, *newpos;
     float4 *geoA;  // (table coordinate, phi, dphi/dd, 1/d)
     float4 *geoB;  // (ux, uy, uz, u = exp(cutoff_lower - d))
     float *g_d;    // [NNP_PARTS][capacity] dE/dd_e, one slot per channel part (summed in k_forces)
@@ -103,41 +105,153 @@ __global__ void k_prep_nodes(TnDev d)
     if (s == d.n - 1) d.sample_ptr[d.n_samples] = d.n;
 }
 
-// Per-edge geometry shared by every layer of the forward and reverse sweeps.
+// Per-edge geometry shared by every layer of the forward and reverse sweeps, written in the
+// MODEL's edge order: each receiver's row is re-sorted by decreasing distance (= increasing table
+// coordinate), so that consecutive edges of a row fall into the same or the next knot interval
+// and the row-walking kernels keep the interval's table data in registers.  One warp per row;
+// the rank of an edge inside its row is found by counting (rows are a few dozen edges).
 // cosine cutoff as radial.py:11-39, u as radial.py:57.
-__global__ void k_edge_geom(TnDev d)
+__global__ void __launch_bounds__(256) k_edge_order(TnDev d)
+{
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= d.n) return;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    const float rl = d.m.cutoff_lower, ru = d.m.cutoff_upper;
+    for (int e = e0 + lane; e < e1; e += 32) {
+        const float dist = d.dists[e];
+        int rank = 0;
+        for (int b = e0; b < e1; ++b) {
+            const float db = __ldg(d.dists + b);
+            rank += (db > dist || (db == dist && b < e)) ? 1 : 0;
+        }
+        if (d.dbg_nosort) rank = e - e0;
+        const int p = e0 + rank;
+        const int i = d.pairs[2 * (size_t)e], j = d.pairs[2 * (size_t)e + 1];
+        const bool loop = (i == j);
+        float phi, dphi;
+        if (rl == 0.0f) {
+            const float x = dist / ru;
+            phi = dist <= ru ? 0.5f * (cospif(x) + 1.0f) : 0.0f;
+            dphi = dist <= ru ? -0.5f * PI_F / ru * sinpif(x) : 0.0f;
+        } else {
+            const float span = ru - rl;
+            const float t = 2.0f * (dist - rl) / span + 1.0f;
+            const bool in = dist >= rl && dist <= ru;
+            phi = in ? 0.5f * (cospif(t) + 1.0f) : 0.0f;
+            dphi = in ? -PI_F / span * sinpif(t) : 0.0f;
+        }
+        const float u = expf(rl - dist);
+        float tx = (u - d.m.u_min) / d.m.u_step;
+        tx = fminf(fmaxf(tx, 0.0f), (float)(d.m.num_knots - 1));
+        const float invd = loop ? 0.0f : 1.0f / dist;
+        d.newpos[e] = p;
+        d.col[p] = d.dbg_col ? i : j;
+        d.geoA[p] = make_float4(tx, phi, dphi, invd);
+        d.geoB[p] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
+                                d.deltas[3 * (size_t)e + 2] * invd, u);
+        for (int q = 0; q < d.nparts; ++q) {
+            d.g_d[(size_t)q * d.capacity + p] = 0.0f;
+            d.g_u[(size_t)q * d.capacity + p] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
+// rev[e] = model-order index of the reverse edge (j <- i) of e = (i <- j): bisection in the
+// sender's row of the caller's list (sorted by sender), mapped through newpos.
+__global__ void k_edge_rev(TnDev d)
 {
     if (overflowed(d)) return;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= d.row_ptr[d.n]) return;
     const int i = d.pairs[2 * (size_t)e], j = d.pairs[2 * (size_t)e + 1];
-    const float dist = d.dists[e];
-    const bool loop = (i == j);
-    const float rl = d.m.cutoff_lower, ru = d.m.cutoff_upper;
-    float phi, dphi;
-    if (rl == 0.0f) {
-        const float x = dist / ru;
-        phi = dist <= ru ? 0.5f * (cospif(x) + 1.0f) : 0.0f;
-        dphi = dist <= ru ? -0.5f * PI_F / ru * sinpif(x) : 0.0f;
-    } else {
-        const float span = ru - rl;
-        const float t = 2.0f * (dist - rl) / span + 1.0f;
-        const bool in = dist >= rl && dist <= ru;
-        phi = in ? 0.5f * (cospif(t) + 1.0f) : 0.0f;
-        dphi = in ? -PI_F / span * sinpif(t) : 0.0f;
+    int lo = d.row_ptr[j], hi = d.row_ptr[j + 1] - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (d.pairs[2 * (size_t)mid + 1] < i) lo = mid + 1; else hi = mid;
     }
-    const float u = expf(rl - dist);
-    float tx = (u - d.m.u_min) / d.m.u_step;
-    tx = fminf(fmaxf(tx, 0.0f), (float)(d.m.num_knots - 1));
-    const float invd = loop ? 0.0f : 1.0f / dist;
-    d.col[e] = j;
-    d.geoA[e] = make_float4(tx, phi, dphi, invd);
-    d.geoB[e] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
-                            d.deltas[3 * (size_t)e + 2] * invd, u);
-    for (int p = 0; p < d.nparts; ++p) {
-        d.g_d[(size_t)p * d.capacity + e] = 0.0f;
-        d.g_u[(size_t)p * d.capacity + e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    d.rev[d.newpos[e]] = d.newpos[lo];
+}
+
+// Radial tables: per knot the values and (knot-spacing-scaled) slopes of the 3 radial functions,
+// [knot][value|slope][3][C].  A row walker keeps the two knots of its current interval in
+// registers; rows are sorted by table coordinate, so moving on means "same interval" (no load),
+// "next interval" (one knot) or a jump (two knots) - a warp-uniform decision.
+template <int C, int CPL>
+struct KnotCache {
+    float v0[3][CPL], m0[3][CPL], v1[3][CPL], m1[3][CPL];
+    int kn;
+
+    __device__ __forceinline__ void init() { kn = -4; }
+
+    __device__ __forceinline__ static void load_knot(const float *__restrict__ tab, int knot, int cb,
+                                                     float (&v)[3][CPL], float (&m)[3][CPL])
+    {
+        const float *row = tab + (size_t)knot * (6 * C) + cb;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ldv<CPL>(row + k * C, v[k]);
+            ldv<CPL>(row + (3 + k) * C, m[k]);
+        }
     }
+
+    __device__ __forceinline__ void seek(const float *__restrict__ tab, int k, int cb)
+    {
+        if (k == kn) return;
+        if (k == kn + 1) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) {
+                    v0[q][v] = v1[q][v];
+                    m0[q][v] = m1[q][v];
+                }
+        } else {
+            load_knot(tab, k, cb, v0, m0);
+        }
+        load_knot(tab, k + 1, cb, v1, m1);
+        kn = k;
+    }
+
+    // value of radial function k at t in [0,1) of the current interval
+    __device__ __forceinline__ void value(const Hermite &h, int k, float (&f)[CPL]) const
+    {
+#pragma unroll
+        for (int v = 0; v < CPL; ++v)
+            f[v] = fmaf(h.h00, v0[k][v], fmaf(h.h10, m0[k][v], fmaf(h.h01, v1[k][v], h.h11 * m1[k][v])));
+    }
+    // d/dt
+    __device__ __forceinline__ void slope(const Hermite &h, int k, float (&df)[CPL]) const
+    {
+#pragma unroll
+        for (int v = 0; v < CPL; ++v)
+            df[v] = fmaf(h.d00, v0[k][v], fmaf(h.d10, m0[k][v], fmaf(h.d01, v1[k][v], h.d11 * m1[k][v])));
+    }
+};
+
+__device__ __forceinline__ int knot_of(float tx, int num_knots, float &t)
+{
+    int kn = (int)tx;
+    kn = kn > num_knots - 2 ? num_knots - 2 : kn;
+    t = tx - (float)kn;
+    return kn;
+}
+
+// Sum of four per-lane partials over the warp with 6 shuffles: returns, in lanes 0 / 16 / 8 / 24,
+// the warp totals of p0 / p1 / p2 / p3 (other lanes hold partial garbage).
+__device__ __forceinline__ float warp_sum4(float p0, float p1, float p2, float p3, int lane)
+{
+    float a = (lane & 16) ? p1 : p0, b = (lane & 16) ? p0 : p1;
+    a += __shfl_xor_sync(NNP_FULL_MASK, b, 16);
+    float c = (lane & 16) ? p3 : p2, e = (lane & 16) ? p2 : p3;
+    c += __shfl_xor_sync(NNP_FULL_MASK, e, 16);
+    float x = (lane & 8) ? c : a;
+    const float y = (lane & 8) ? a : c;
+    x += __shfl_xor_sync(NNP_FULL_MASK, y, 8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(NNP_FULL_MASK, x, o);
+    return x;
 }
 
 // Lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coordinate).
@@ -216,7 +330,7 @@ __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
         float zsnd[CPL];
         ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, false>(d.m.tables, d.m.num_knots, ga.x, cb, f, df);
+        table_lookup<C, CPL, false>(d.m.tables_mono, d.m.num_knots, ga.x, cb, f, df);
         float b[9];
         edge_basis9(gb.x, gb.y, gb.z, b);
 #pragma unroll
@@ -414,7 +528,7 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
     const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
     const int cb = part * 32 * CPL + lane * CPL;
-    const float *tab = d.m.tables + (size_t)(layer + 1) * (d.m.num_knots - 1) * 12 * C;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
     const float *Y = d.Yc[layer];
     float acc[9][CPL];
 #pragma unroll
@@ -422,21 +536,49 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
 #pragma unroll
         for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
-#pragma unroll 2
+    KnotCache<C, CPL> kc;
+    kc.init();
+    const int nk = d.m.num_knots;
+    // software pipeline: the sender row of edge e+1 is in flight while edge e is consumed
+    float y[9][CPL];
+    float4 ga = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e0 < e1) {
+        ga = d.geoA[e0];
+        const float *yj = Y + (size_t)d.col[e0] * 9 * C + cb;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ldv<CPL>(yj + q * C, y[q]);
+    }
     for (int e = e0; e < e1; ++e) {
-        const int j = d.col[e];
-        const float4 ga = d.geoA[e];
-        float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, false>(tab, d.m.num_knots, ga.x, cb, f, df);
-        const float *yj = Y + (size_t)j * 9 * C + cb;
+        float yn[9][CPL];
+        float4 gan = ga;
+        if (e + 1 < e1) {
+            gan = d.geoA[e + 1];
+            const float *yj = Y + (size_t)d.col[e + 1] * 9 * C + cb;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            float y[CPL];
-            ldv<CPL>(yj + q * C, y);
-            const int grp = group_of(q);
-#pragma unroll
-            for (int v = 0; v < CPL; ++v) acc[q][v] += (f[grp][v] * ga.y) * y[v];
+            for (int q = 0; q < 9; ++q) ldv<CPL>(yj + q * C, yn[q]);
         }
+        float t;
+        const int kn = knot_of(ga.x, nk, t);
+        kc.seek(tab, kn, cb);
+        const float phi = ga.y;
+        const Hermite h = hermite_weights(t);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float f[CPL];
+            kc.value(h, k, f);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) f[v] *= phi;
+            const int qa = k == 0 ? 0 : (k == 1 ? 1 : 4), qb = k == 0 ? 1 : (k == 1 ? 4 : 9);
+#pragma unroll
+            for (int q = qa; q < qb; ++q)
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) acc[q][v] = fmaf(f[v], y[q][v], acc[q][v]);
+        }
+        ga = gan;
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) y[q][v] = yn[q][v];
     }
     float *out = d.Mc[layer] + (size_t)s * 9 * C + cb;
 #pragma unroll
@@ -463,6 +605,162 @@ __global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
     for (int q = 0; q < 9; ++q) stv<CPL>(qo + q * C, qv[q]);
 }
 
+// Knot cache restricted to the radial functions [K0, K0 + NG) (see KnotCache).
+template <int C, int CPL, int K0, int NG>
+struct KnotCacheG {
+    float v0[NG][CPL], m0[NG][CPL], v1[NG][CPL], m1[NG][CPL];
+    int kn;
+    __device__ __forceinline__ void init() { kn = -4; }
+    __device__ __forceinline__ static void load_knot(const float *__restrict__ tab, int knot, int cb,
+                                                     float (&v)[NG][CPL], float (&m)[NG][CPL])
+    {
+        const float *row = tab + (size_t)knot * (6 * C) + cb;
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            ldv<CPL>(row + (K0 + k) * C, v[k]);
+            ldv<CPL>(row + (3 + K0 + k) * C, m[k]);
+        }
+    }
+    __device__ __forceinline__ void seek(const float *__restrict__ tab, int k, int cb)
+    {
+        if (k == kn) return;
+        if (k == kn + 1) {
+#pragma unroll
+            for (int q = 0; q < NG; ++q)
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) {
+                    v0[q][v] = v1[q][v];
+                    m0[q][v] = m1[q][v];
+                }
+        } else {
+            load_knot(tab, k, cb, v0, m0);
+        }
+        load_knot(tab, k + 1, cb, v1, m1);
+        kn = k;
+    }
+    __device__ __forceinline__ void value(const Hermite &h, int k, float (&f)[CPL]) const
+    {
+#pragma unroll
+        for (int v = 0; v < CPL; ++v)
+            f[v] = fmaf(h.h00, v0[k][v], fmaf(h.h10, m0[k][v], fmaf(h.h01, v1[k][v], h.h11 * m1[k][v])));
+    }
+    __device__ __forceinline__ void slope(const Hermite &h, int k, float (&df)[CPL]) const
+    {
+#pragma unroll
+        for (int v = 0; v < CPL; ++v)
+            df[v] = fmaf(h.d00, v0[k][v], fmaf(h.d10, m0[k][v], fmaf(h.d01, v1[k][v], h.d11 * m1[k][v])));
+    }
+};
+
+// One warp's share of a receiver row: components [Q0, Q0 + NQ) = radial groups [K0, K0 + NG).
+template <int C, int CPL, int K0, int NG, int Q0, int NQ>
+__device__ __forceinline__ void message_row_part(const TnDev &d, const float *__restrict__ tab,
+                                                 const float *__restrict__ Y, float *__restrict__ Mout,
+                                                 int s, int cb)
+{
+    float acc[NQ][CPL];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    KnotCacheG<C, CPL, K0, NG> kc;
+    kc.init();
+    const int nk = d.m.num_knots;
+    int j = e0 < e1 ? d.col[e0] : 0;
+    float4 ga = e0 < e1 ? d.geoA[e0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = e0; e < e1; ++e) {
+        const float *yj = Y + ((size_t)j * 9 + Q0) * C + cb;
+        float y[NQ][CPL];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ldv<CPL>(yj + q * C, y[q]);
+        float t;
+        const int kn = knot_of(ga.x, nk, t);
+        kc.seek(tab, kn, cb);
+        const float phi = ga.y;
+        if (e + 1 < e1) {
+            j = d.col[e + 1];
+            ga = d.geoA[e + 1];
+        }
+        const Hermite h = hermite_weights(t);
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            float f[CPL];
+            kc.value(h, k, f);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) f[v] *= phi;
+            // local component range of group K0 + k
+            const int g = K0 + k;
+            const int qa = (g == 0 ? 0 : (g == 1 ? 1 : 4)) - Q0, qb = (g == 0 ? 1 : (g == 1 ? 4 : 9)) - Q0;
+#pragma unroll
+            for (int q = qa; q < qb; ++q)
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) acc[q][v] = fmaf(f[v], y[q][v], acc[q][v]);
+        }
+    }
+    float *out = Mout + ((size_t)s * 9 + Q0) * C + cb;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+// M_i = sum_e f_e[:,grp] * Yc_j with two warps per (receiver, channel part): one owns the I and A
+// components (4 of 9), the other the S components (5 of 9), so each keeps only its own groups'
+// knot data and accumulators in registers.  The node update Q = (M*Y + Y*M)/(|.|^2 + 1) follows
+// after a block barrier, the two warps taking half of the lane's channels each.
+template <int C, int CPL>
+__global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
+{
+    constexpr int NPARTS = C / (32 * CPL);
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / (2 * NPARTS), rem = gw - s * (2 * NPARTS);
+    const int part = rem >> 1, half = rem & 1;
+    const bool live = s < d.n;
+    const int cb = part * 32 * CPL + lane * CPL;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    const float *Y = d.Yc[layer];
+    float *M = d.Mc[layer];
+    if (live) {
+        if (half == 0) message_row_part<C, CPL, 0, 2, 0, 4>(d, tab, Y, M, s, cb);
+        else message_row_part<C, CPL, 2, 1, 4, 5>(d, tab, Y, M, s, cb);
+    }
+    __syncthreads();   // the partner warp's components of M are visible now
+    if (!live) return;
+    constexpr int HC = CPL >= 2 ? CPL / 2 : 1;      // channels per lane in the node update
+    if (CPL == 1 && half == 1) return;
+    const int cq = cb + (CPL >= 2 ? half * HC : 0);
+    const float *mi = M + (size_t)s * 9 * C + cq;
+    const float *yi = Y + (size_t)s * 9 * C + cq;
+    float mv[9][HC], yv[9][HC], qv[9][HC];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        if constexpr (HC == 2) {
+            const float2 a = *reinterpret_cast<const float2 *>(mi + q * C);   // written this launch: no __ldg
+            mv[q][0] = a.x;
+            mv[q][1] = a.y;
+        } else {
+            mv[q][0] = mi[q * C];
+        }
+        ldv<HC>(yi + q * C, yv[q]);
+    }
+#pragma unroll
+    for (int v = 0; v < HC; ++v) {
+        float m9[9], y9[9], q9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            m9[q] = mv[q][v];
+            y9[q] = yv[q][v];
+        }
+        node_product_fwd(m9, y9, q9);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) qv[q][v] = q9[q];
+    }
+    float *qo = d.Qc + (size_t)s * 9 * C + cq;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<HC>(qo + q * C, qv[q]);
+}
+
 // Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
 // is a gather over a's own row):
 //   G_Y[a] += sum_e f_e[:,grp] * G_M[b]                         (b = sender of e)
@@ -482,7 +780,7 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
     const int s = gw / NPARTS, part = gw - s * NPARTS;
     if (s >= d.n) return;
     const int cb = part * 32 * CPL + lane * CPL;
-    const float *tab = d.m.tables + (size_t)(layer + 1) * (d.m.num_knots - 1) * 12 * C;
+    const float *tab = d.m.tables_mono + (size_t)(layer + 1) * (d.m.num_knots - 1) * 12 * C;
     float yown[9][CPL], acc[9][CPL];
     {
         const float *p = d.Yc[layer] + (size_t)s * 9 * C + cb;
@@ -829,7 +1127,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         float zsnd[CPL];
         ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
-        table_lookup<C, CPL, true>(d.m.tables, d.m.num_knots, ga.x, cb, f, df);
+        table_lookup<C, CPL, true>(d.m.tables_mono, d.m.num_knots, ga.x, cb, f, df);
         float b[9];
         edge_basis9(gb.x, gb.y, gb.z, b);
         const float su = -gb.w * inv_step * ga.y;
@@ -863,7 +1161,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
 }
 
 // forces: F_i = -sum_{e in row i} [ (g_d[e] + g_d[e']) u_e + (1 - u u^T)(g_u[e] - g_u[e']) / d_e ]
-// with e' the reverse edge (u_e' = -u_e), found by bisection in the sender's sorted row.
+// with e' the reverse edge (u_e' = -u_e), precomputed by k_edge_rev.
 __global__ void k_forces(TnDev d)
 {
     if (overflowed(d)) return;
@@ -874,12 +1172,7 @@ __global__ void k_forces(TnDev d)
     for (int e = e0; e < e1; ++e) {
         const int j = d.col[e];
         if (j == s) continue;
-        int lo = d.row_ptr[j], hi = d.row_ptr[j + 1] - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (d.col[mid] < s) lo = mid + 1; else hi = mid;
-        }
-        const int er = lo;
+        const int er = d.rev[e];
         const float4 ga = d.geoA[e];
         const float4 gb = d.geoB[e];
         float gd = 0.0f, vx = 0.0f, vy = 0.0f, vz = 0.0f;
@@ -916,6 +1209,8 @@ size_t carve(TnDev &d, void *ws)
     const size_t T = n * 9 * C;
     const int L = d.m.num_layers;
     d.col = ar.take<int>(cap);
+    d.rev = ar.take<int>(cap);
+    d.newpos = ar.take<int>(cap);
     d.geoA = ar.take<float4>(cap);
     d.geoB = ar.take<float4>(cap);
     d.g_d = ar.take<float>(cap * NNP_PARTS);
@@ -1018,7 +1313,7 @@ GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n,
 // node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
 // through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
 struct EdgeTuning {
-    int emb, fwd, bwd, embbwd, bwd_block;
+    int emb, fwd, bwd, embbwd, bwd_block, fwd_block;
 };
 static int env_int(const char *name, int fallback)
 {
@@ -1029,7 +1324,7 @@ static const EdgeTuning &edge_tuning()
 {
     static const EdgeTuning t = {env_int("NNP_CPL_EMB", 2), env_int("NNP_CPL_FWD", 4),
                                  env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
-                                 env_int("NNP_BWD_BLOCK", 128)};
+                                 env_int("NNP_BWD_BLOCK", 128), env_int("NNP_FWD_BLOCK", 128)};
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -1054,6 +1349,12 @@ int run_step(TnDev &d, cudaStream_t st)
     const int ew_blocks = nnp_blocks((int64_t)n * C, 256);
     const nnp_tn_model &m = d.m;
     const EdgeTuning &tune = edge_tuning();
+    static const int dbg_kn = env_int("NNP_DBG_KN", 0);
+    if (dbg_kn) d.m.num_knots = 2;
+    static const int dbg_col = env_int("NNP_DBG_COL", 0);
+    d.dbg_col = dbg_col;
+    static const int dbg_nosort = env_int("NNP_DBG_NOSORT", 0);
+    d.dbg_nosort = dbg_nosort;   // measurement only: every edge reads table interval 0
     {
         auto parts = [](int cpl) {
             if (cpl * 32 > C) cpl = C / 32;
@@ -1071,7 +1372,8 @@ int run_step(TnDev &d, cudaStream_t st)
 
     { NNP_PROF("k_fill_int", st); k_fill_int<<<NNP_GRID(nnp_blocks(d.n_samples + 1, 256)), 256, 0, st>>>(d.sample_ptr, d.n_samples + 1, n); }
     { NNP_PROF("k_prep_nodes", st); k_prep_nodes<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d); }
-    { NNP_PROF("k_edge_geom", st); k_edge_geom<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
+    { NNP_PROF("k_edge_order", st); k_edge_order<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
+    { NNP_PROF("k_edge_rev", st); k_edge_rev<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
 
     // ---- embedding
     { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d))); }
@@ -1092,7 +1394,9 @@ int run_step(TnDev &d, cudaStream_t st)
         if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
-        { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, l))); }
+        static const int fwd_split = env_int("NNP_FWD_SPLIT", 1);
+        if (fwd_split) { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); }
+        else { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); } 
         GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + 3, d.Dc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
         { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, l + 1 < L ? d.Xh[l + 1] : nullptr, l + 1 < L ? d.nx[l + 1] : nullptr, n, C); }

@@ -126,10 +126,10 @@ def build_radial_tables(params: Dict[str, np.ndarray], config: TNConfig):
     depend on the edge only through d, so they are 1-D functions R -> R^{3C}; the expnorm basis
     is a set of equal-width Gaussians in u, which makes u the natural abscissa (uniform knots
     resolve every basis function equally).  Values and u-derivatives are computed in float64
-    (derivative by forward mode through the MLP); the cubic Hermite interpolant of each knot
-    interval is stored as monomial coefficients for Horner evaluation on the device:
-    ``tables[t, k, p, j, c]`` = coefficient of x^p (x in [0, 1] across interval k) of output j of
-    channel c.  Returns (tables float32, u_min, u_step, max interpolation error measured at the
+    (derivative by forward mode through the MLP); the device evaluates the cubic Hermite
+    interpolant of a knot interval from the data of its two knots:
+    ``tables[t, k, p, j, c]`` = value (p = 0) or slope times the knot spacing (p = 1) at knot k of
+    output j of channel c.  Returns (tables float32, u_min, u_step, max interpolation error measured at the
     interval midpoints relative to the largest table value).
     """
     C, K, L, nk = config.embedding_dimension, config.num_rbf, config.num_layers, config.num_knots
@@ -157,22 +157,27 @@ def build_radial_tables(params: Dict[str, np.ndarray], config: TNConfig):
 
     knots = u_min + u_step * np.arange(nk)
     at_knots = evaluate(knots)
-    tables = np.empty((L + 1, nk - 1, 4, 3, C), dtype=np.float64)
+    tables = np.empty((L + 1, nk, 2, 3, C), dtype=np.float64)
     for t, (f, df) in enumerate(at_knots):
-        f0, f1 = f[:-1], f[1:]
-        m0, m1 = df[:-1] * u_step, df[1:] * u_step
-        tables[t, :, 0] = f0
-        tables[t, :, 1] = m0
-        tables[t, :, 2] = 3.0 * (f1 - f0) - 2.0 * m0 - m1
-        tables[t, :, 3] = 2.0 * (f0 - f1) + m0 + m1
-    # interpolation error at the interval midpoints
+        tables[t, :, 0] = f
+        tables[t, :, 1] = df * u_step
+    # interpolation error at the interval midpoints (Hermite weights at x = 1/2)
     mid = evaluate(knots[:-1] + 0.5 * u_step)
     err = 0.0
     for t, (f, _) in enumerate(mid):
         c = tables[t]
-        interp = c[:, 0] + 0.5 * c[:, 1] + 0.25 * c[:, 2] + 0.125 * c[:, 3]
+        interp = 0.5 * (c[:-1, 0] + c[1:, 0]) + 0.125 * (c[:-1, 1] - c[1:, 1])
         err = max(err, float(np.max(np.abs(interp - f)) / max(np.max(np.abs(c[:, 0])), 1e-30)))
     return tables.astype(np.float32), u_min, u_step, err
+
+
+def monomial_tables(tables: np.ndarray) -> np.ndarray:
+    """Knot data [T, nk, 2, 3, C] -> per-interval monomial coefficients [T, nk-1, 4, 3, C] of the
+    same cubic Hermite interpolants (expanded in float64)."""
+    t = tables.astype(np.float64)
+    f0, f1, m0, m1 = t[:, :-1, 0], t[:, 1:, 0], t[:, :-1, 1], t[:, 1:, 1]
+    mono = np.stack([f0, m0, 3.0 * (f1 - f0) - 2.0 * m0 - m1, 2.0 * (f0 - f1) + m0 + m1], axis=2)
+    return mono.astype(np.float32)
 
 
 def gemm_tile_n(n_out: int) -> int:
@@ -268,6 +273,7 @@ class TensorNet:
         m.z_recv = dev("z_recv", P["emb"] @ Wa.T)
         m.z_send = dev("z_send", P["emb"] @ Wb.T + P["emb2_b"])
         m.tables = dev("tables", tables)
+        m.tables_mono = dev("tables_mono", monomial_tables(tables))
         m.init_norm_g, m.init_norm_b = dev("ing", P["init_norm_g"]), dev("inb", P["init_norm_b"])
 
         def gemm_weight(slot, name, w):

@@ -116,15 +116,18 @@ def test_radial_tables_reproduce_the_mlp(rl):
     cfg = P.TNConfig(embedding_dimension=32, num_layers=2, num_rbf=16, cutoff_lower=rl, cutoff_upper=4.5)
     params = P.init_params(cfg, 7)
     tables, u_min, u_step, err = P.build_radial_tables(params, cfg)
-    assert tables.shape == (3, cfg.num_knots - 1, 4, 3, 32) and err < 1e-6
+    assert tables.shape == (3, cfg.num_knots, 2, 3, 32) and err < 1e-6
     d = np.random.default_rng(0).uniform(max(rl, 0.0), 4.5, 4000)
     u = np.exp(rl - d)
     x = (u - u_min) / u_step
     k = np.clip(np.floor(x).astype(int), 0, cfg.num_knots - 2)
     t = (x - k)[:, None, None]
-    c = tables.astype(np.float64)[:, k]                      # [tables, edges, 4, 3, C]
-    val = ((c[:, :, 3] * t + c[:, :, 2]) * t + c[:, :, 1]) * t + c[:, :, 0]
-    dval = ((3 * c[:, :, 3] * t + 2 * c[:, :, 2]) * t + c[:, :, 1]) / u_step * (-u)[:, None, None]
+    a, b = tables.astype(np.float64)[:, k], tables.astype(np.float64)[:, k + 1]   # [tables, edges, 2, 3, C]
+    t2, t3 = t * t, t * t * t
+    val = ((2 * t3 - 3 * t2 + 1) * a[:, :, 0] + (t3 - 2 * t2 + t) * a[:, :, 1]
+           + (-2 * t3 + 3 * t2) * b[:, :, 0] + (t3 - t2) * b[:, :, 1])
+    dval = ((6 * t2 - 6 * t) * a[:, :, 0] + (3 * t2 - 4 * t + 1) * a[:, :, 1]
+            + (-6 * t2 + 6 * t) * b[:, :, 0] + (3 * t2 - 2 * t) * b[:, :, 1]) / u_step * (-u)[:, None, None]
     rho = O.rbf_expnorm(d, params["rbf_means"], params["rbf_betas"], rl)
     drho = O.rbf_expnorm_dd(d, params["rbf_means"], params["rbf_betas"], rl)
     for l in range(2):

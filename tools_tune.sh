@@ -1,5 +1,6 @@
 #!/bin/bash
-timeout 200 python -m pytest tests/test_gpu_tensornet.py -q -x -k "gemm or periodic_triclinic or config_a" --timeout 150 -p no:cacheprovider 2>&1 | tail -3
-for DBG in 0 512; do
-  NNP_GEMM_DBG=$DBG NNP_GEMM_MODE=4 timeout 200 python tools_tune.py C 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['env'], d['wl'], d['graph_ms'], 'gemm_mix', d['top'].get('gemm_mix'), 'dense', d['top'].get('gemm_dense'))"
-done
+timeout 600 python -m pytest tests/test_gpu_tensornet.py -x -q --timeout 300 -p no:cacheprovider 2>&1 | tail -2
+run() { env "$@" timeout 200 python tools_tune.py C 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['env'], d['graph_ms'], d['E'], {k:v for k,v in d['top'].items() if 'edge' in k})"; }
+run NNP_FWD_BLOCK=128
+run NNP_FWD_BLOCK=128 NNP_DBG_NOSORT=1
+run NNP_FWD_BLOCK=64
