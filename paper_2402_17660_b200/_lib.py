@@ -73,6 +73,9 @@ class TnModel(ctypes.Structure):
 _lib = None
 
 
+DEFAULT_GEMM_MODE = 5   # streaming tcgen05 kernel for the 128 x 128 mixes, per-tile tcgen05 otherwise
+
+
 def load() -> ctypes.CDLL:
     """Load the extension once; fail loudly when it is absent."""
     global _lib

@@ -835,6 +835,323 @@ static int launch_wstat(const GemmBatch &b, int count, cudaStream_t stream)
     return NNP_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Streaming kernel for the channel-mixing GEMMs (N = K = 128), mode 5: the one the step uses.
+//
+//   out^T[n, r] = sum_k W[n, k] * X[r, k]
+//
+// The mixes are skinny (M = 9 N_atoms rows against a 128 x 128 weight): 217 MB of HBM traffic and
+// 29 us of 3xTF32 tensor time each at config C, i.e. bound by how many bytes are kept in flight.
+//   * persistent CTAs bound to one component group; its weight is the MMA's A operand and lives
+//     in TENSOR MEMORY for the life of the CTA (TF32 hi part in columns [0,128), lo in [128,256);
+//     lane = output channel), so all of shared memory is an activation ring;
+//   * activation rows are copied global -> shared with cp.async (16 B per request, written
+//     straight into the K-major SWIZZLE_128B layout, no register staging) through a 7-stage
+//     ring, five 32-column chunks (80 KB) ahead of the tensor core.  The copied FP32 words ARE
+//     the "hi" operand (kind::tf32 reads the top 19 bits); the producer only derives
+//     lo = x - trunc_tf32(x);
+//   * one thread issues the tcgen05.mma triples into one of two TMEM accumulators ([256,384),
+//     [384,512)); four epilogue warps drain the other with tcgen05.ld.  Lane = output channel, so
+//     the 32 lanes of a warp hold 32 consecutive channels of one row: every store instruction
+//     writes one full 128-byte line, no staging tile.
+constexpr int ST_STAGES = 7;
+constexpr int ST_LAG = 5;                           // chunks in flight behind the newest request
+constexpr int ST_PRODUCERS = 256;
+constexpr int ST_THREADS = 128 + 32 + ST_PRODUCERS;
+constexpr int ST_STAGE_BYTES = 2 * BM * 128;        // raw (= hi) and lo, 128 rows x 128 B each
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
+template <int N_>
+__device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory");
+}
+
+template <int PRO, int EPI>
+__global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch batch, WstatSchedule sched)
+{
+    constexpr int N = 128, K = 128, NCHUNK = K / KC;
+    extern __shared__ char smem_raw[];
+    char *ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint64_t full_bar[ST_STAGES], empty_bar[ST_STAGES], tfull_bar[2], tempty_bar[2];
+    __shared__ uint32_t tmem_base_s;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int z = 0;
+    while (z < 2 && (int)blockIdx.x >= sched.cta_begin[z + 1]) ++z;
+    const int my = blockIdx.x - sched.cta_begin[z];
+    const int stride = sched.cta_begin[z + 1] - sched.cta_begin[z];
+    const GemmArgs &g = batch.g[z];
+    const int tiles = (g.M + BM - 1) / BM;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST_STAGES; ++s) {
+            mbar_init(&full_bar[s], ST_PRODUCERS);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull_bar[a], 1);
+            mbar_init(&tempty_bar[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = tmem_base_s;
+
+    // weights -> tensor memory (once): lane = output channel n, column k (hi) / 128 + k (lo)
+    if (warp < 4) {
+        const int n = warp * 32 + lane;
+        const float *wrow = g.W + (size_t)n * K;
+        const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+        for (int k0 = 0; k0 < K; k0 += 16) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(wrow + k0 + 4 * q));
+                tf32_split(v.x, hi[4 * q], lo[4 * q]);
+                tf32_split(v.y, hi[4 * q + 1], lo[4 * q + 1]);
+                tf32_split(v.z, hi[4 * q + 2], lo[4 * q + 2]);
+                tf32_split(v.w, hi[4 * q + 3], lo[4 * q + 3]);
+            }
+            tmem_st16(lane_addr + (uint32_t)k0, hi);
+            tmem_st16(lane_addr + (uint32_t)(K + k0), lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    if (warp >= 5) {
+        // ============================================================ producers (256 threads)
+        const int ptid = tid - 160;
+        constexpr int PIECES = BM * 8 / ST_PRODUCERS;       // 16-byte pieces per thread per chunk (4)
+        const int total = ((tiles - my + stride - 1) / stride) * NCHUNK;
+        uint32_t off[PIECES];
+#pragma unroll
+        for (int p = 0; p < PIECES; ++p) {
+            const int idx = ptid + p * ST_PRODUCERS;
+            off[p] = swz(idx >> 3, idx & 7);
+        }
+        auto issue = [&](int it) {
+            const int s = it % ST_STAGES;
+            const uint32_t ph = (uint32_t)((it / ST_STAGES) & 1);
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            const int tile = my + (it / NCHUNK) * stride;
+            const int k0 = (it % NCHUNK) * KC;
+            const uint32_t raw = smem_u32(ring + s * ST_STAGE_BYTES);
+#pragma unroll
+            for (int p = 0; p < PIECES; ++p) {
+                const int idx = ptid + p * ST_PRODUCERS;
+                const int r = tile * BM + (idx >> 3);
+                const bool ok = r < g.M;
+                const float *src = g.A + (size_t)gemm_phys_row(g, ok ? r : 0) * g.lda + k0 + (idx & 7) * 4;
+                cp_async16(raw + off[p], src, ok ? 16u : 0u);   // rows past the end are zero-filled
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        auto convert = [&](int it) {
+            const int s = it % ST_STAGES;
+            char *x_hi = ring + s * ST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
+#pragma unroll
+            for (int p = 0; p < PIECES; ++p) {
+                float4 v = *reinterpret_cast<const float4 *>(x_hi + off[p]);
+                if (PRO == PRO_SILU) {
+                    v.x = nnp_silu(v.x);
+                    v.y = nnp_silu(v.y);
+                    v.z = nnp_silu(v.z);
+                    v.w = nnp_silu(v.w);
+                    *reinterpret_cast<float4 *>(x_hi + off[p]) = v;
+                }
+                uint4 l;
+                l.x = __float_as_uint(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+                l.y = __float_as_uint(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+                l.z = __float_as_uint(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+                l.w = __float_as_uint(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+                *reinterpret_cast<uint4 *>(x_lo + off[p]) = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&full_bar[s]);
+        };
+        for (int it = 0; it < total + ST_LAG; ++it) {
+            if (it < total) issue(it);
+            else asm volatile("cp.async.commit_group;" ::: "memory");   // keep the group count uniform
+            if (it >= ST_LAG) {
+                cp_async_wait<ST_LAG>();            // everything but the newest ST_LAG groups has landed
+                convert(it - ST_LAG);
+            }
+        }
+    } else if (warp == 4) {
+        // ================================================================ MMA issue (1 thread)
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(N);
+            int it = 0, tcount = 0;
+            for (int tile = my; tile < tiles; tile += stride, ++tcount) {
+                const int acc = tcount & 1;
+                const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+                mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t tmem_d = tmem_base + (uint32_t)(2 * K + acc * N);
+                for (int c = 0; c < NCHUNK; ++c, ++it) {
+                    const int s = it % ST_STAGES;
+                    const uint32_t ph = (uint32_t)((it / ST_STAGES) & 1);
+                    char *x_hi = ring + s * ST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
+                    mbar_wait(&full_bar[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t dx_hi = make_desc(smem_u32(x_hi)), dx_lo = make_desc(smem_u32(x_lo));
+#pragma unroll
+                    for (int ks = 0; ks < KC / 8; ++ks) {
+                        const uint64_t adv = (uint64_t)(ks * 32 >> 4);
+                        const uint32_t kcol = (uint32_t)(c * KC + ks * 8);
+                        umma_tf32_ta(tmem_d, tmem_base + K + kcol, dx_hi + adv, idesc, (c | ks) != 0);  // W_lo * X_hi
+                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_lo + adv, idesc, 1);                  // W_hi * X_lo
+                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_hi + adv, idesc, 1);                  // W_hi * X_hi
+                    }
+                    umma_commit(&empty_bar[s]);
+                    if (c + 1 == NCHUNK) umma_commit(&tfull_bar[acc]);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ==================================================================== epilogue (warps 0-3)
+        // Four warps, one per scheduler, have nothing to hide latency behind, so the per-element
+        // work is a pointer bump: rows of a tile are walked in order and the [node][9][C]
+        // addressing (ncomp rows per node, then a skip of 9 - ncomp rows) is kept incrementally.
+        const int n = warp * 32 + lane;                     // accumulator lane = output channel
+        const int ncomp = g.ncomp;
+        const int wrap = ncomp > 0 ? ncomp : 0x7fffffff;
+        const int ldo = g.ldo;
+        const int skip = ncomp > 0 ? (9 - ncomp) * ldo : 0;
+        const float bias = g.bias ? __ldg(g.bias + n) : 0.0f;
+        int tcount = 0;
+        for (int tile = my; tile < tiles; tile += stride, ++tcount) {
+            const int acc = tcount & 1;
+            const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
+            const int r0 = tile * BM;
+            const int rows = g.M - r0 < BM ? g.M - r0 : BM;
+            int node = node_of(ncomp, r0);
+            int comp = ncomp > 0 ? r0 - node * ncomp : 0;
+            const size_t prow = ncomp > 0 ? (size_t)node * 9 + g.q0 + comp : (size_t)r0;
+            float *po = g.out + prow * ldo + n;             // element (row r0, channel n); ldaux == ldo
+            float *po2 = EPI == EPI_GATE ? g.out2 + prow * ldo + n : nullptr;
+            const float *pa = (EPI == EPI_ADD || EPI == EPI_MUL_SILU_GRAD) ? g.aux + prow * ldo + n : nullptr;
+            const float *pg = EPI == EPI_GATE ? g.aux + (size_t)node * g.ldaux + 3 * n + g.grp : nullptr;
+            int off = 0, goff = 0;                          // running element offsets from po / pg
+            bool waited = false;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BM; c0 += 16) {
+                if (c0 >= rows) break;
+                // addresses of this block's 16 rows, and every global read issued up front
+                int o[16];
+                float a[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    o[i] = off;
+                    a[i] = 0.0f;
+                    if (c0 + i < rows) {
+                        if (EPI == EPI_ADD || EPI == EPI_MUL_SILU_GRAD) a[i] = pa[off];
+                        if (EPI == EPI_GATE) a[i] = __ldg(pg + goff);
+                    }
+                    off += ldo;
+                    if (++comp == wrap) {
+                        comp = 0;
+                        off += skip;
+                        goff += g.ldaux;
+                    }
+                }
+                if (!waited) {
+                    mbar_wait(&tfull_bar[acc], acc_ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    waited = true;
+                }
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(2 * K + acc * N + c0), v);
+                // v[i] = out[row c0 + i][channel n]: the warp's 32 lanes cover one 128-byte line per row
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    if (c0 + i < rows) {
+                        const float x = v[i] + bias;
+                        if (EPI == EPI_STORE) {
+                            po[o[i]] = x;
+                        } else if (EPI == EPI_ADD) {
+                            po[o[i]] = x + a[i];
+                        } else if (EPI == EPI_MUL_SILU_GRAD) {
+                            po[o[i]] = x * nnp_silu_grad(a[i]);
+                        } else {
+                            po2[o[i]] = x;
+                            po[o[i]] = x * nnp_silu(a[i]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&tempty_bar[acc]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512)
+                     : "memory");
+    }
+}
+
+template <int PRO, int EPI>
+static int launch_stream(const GemmBatch &b, int count, cudaStream_t stream)
+{
+    if (count < 1 || count > 3) return -100;
+    for (int i = 0; i < count; ++i)
+        if (b.g[i].N != 128 || b.g[i].K != 128 || b.g[i].lda % 4 != 0 ||
+            ((EPI == EPI_ADD || EPI == EPI_MUL_SILU_GRAD) && b.g[i].ldaux != b.g[i].ldo) ||
+            (int64_t)b.g[i].M * 9 * b.g[i].ldo >= (int64_t)1 << 31)
+            return -100;
+    constexpr int smem = ST_STAGES * ST_STAGE_BYTES + 1024;
+    static int num_sms = 0;
+    if (num_sms == 0) {
+        cudaFuncSetAttribute(gemm_stream_kernel<PRO, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    int tiles[3] = {0, 0, 0}, total = 0;
+    for (int i = 0; i < count; ++i) {
+        tiles[i] = (b.g[i].M + BM - 1) / BM;
+        total += tiles[i];
+    }
+    if (total <= 0) return NNP_OK;
+    // CTAs per problem in proportion to its tiles (at least one, at most one per tile)
+    WstatSchedule sc{};
+    int used = 0;
+    for (int i = 0; i < count; ++i) {
+        int c = (int)(((int64_t)tiles[i] * num_sms) / total);
+        c = std::max(1, std::min(c, tiles[i]));
+        if (tiles[i] == 0) c = 0;
+        sc.cta_begin[i] = used;
+        used += c;
+    }
+    for (int i = count; i < 4; ++i) sc.cta_begin[i] = used;
+    gemm_stream_kernel<PRO, EPI><<<NNP_GRID(used), ST_THREADS, smem, stream>>>(b, sc);
+    NNP_CHECK_LAUNCH("gemm_stream");
+    return NNP_OK;
+}
+
 template <int PRO, int EPI, int NT>
 static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStream_t stream)
 {
@@ -893,6 +1210,7 @@ static int gemm_launch(const GemmBatch &b_in, int count, cudaStream_t stream)
     if (maxM <= 0) return NNP_OK;
     if (g_nnp_gemm_use_mma >= 2) {
         int rc = -100;
+        if (g_nnp_gemm_use_mma == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);
         if (g_nnp_gemm_use_mma == 4) rc = tc5::launch_wstat<PRO, EPI>(b, count, stream);
         if (g_nnp_gemm_use_mma == 2) rc = tc5::launch_ws<PRO, EPI>(b, count, stream);
         if (rc == -100) rc = tc5::launch<PRO, EPI>(b, count, stream);

@@ -22,7 +22,8 @@
 #include "tn_gemm_tc5.cuh"
 #include "tn_math.cuh"
 
-int g_nnp_gemm_use_mma = 3;  // 3 = tcgen05 one tile per CTA (default), 2 = persistent tcgen05, 1 = mma.sync, 0 = FFMA
+int g_nnp_gemm_use_mma = 5;  // 5 = streaming tcgen05 for the 128x128 mixes (default; other shapes use 3), 4 = W in TMEM,
+                              // 3 = tcgen05 one tile per CTA, 2 = persistent tcgen05, 1 = mma.sync, 0 = FFMA
 
 namespace {
 
@@ -1532,7 +1533,7 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 4 ? 4 : use_mma);
+    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 5 ? 5 : use_mma);
     return NNP_OK;
 }
 

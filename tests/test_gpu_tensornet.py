@@ -49,7 +49,7 @@ def check(model, z, pos, batch, box, e_tol=E_TOL, f_tol=F_TOL):
     return e_err, f_err
 
 
-@pytest.mark.parametrize("mode", [4, 2, 3, 1, 0])
+@pytest.mark.parametrize("mode", [5, 4, 2, 3, 1, 0])
 def test_gemm_tile_engine(mode):
     """All inner loops (weight-stationary tcgen05 with W in TMEM, persistent tcgen05, per-tile tcgen05,
     mma.sync, FFMA) against float64."""
@@ -73,7 +73,7 @@ def test_gemm_tile_engine(mode):
             err = (out.double() - ref).abs().max().item() / ref.abs().max().item()
             assert err < 5e-6, (mode, M, N, K, err)   # FP32-level accuracy from the 3xTF32 split
     finally:
-        lib.nnp_set_gemm_mode(3)
+        lib.nnp_set_gemm_mode(_lib.DEFAULT_GEMM_MODE)
 
 
 def small_open(rng, n=20):
@@ -92,7 +92,7 @@ def test_small_open_system(rng, C, L):
     check(model, *small_open(rng))
 
 
-@pytest.mark.parametrize("gemm_mode", [4, 2, 3, 1, 0])
+@pytest.mark.parametrize("gemm_mode", [5, 4, 2, 3, 1, 0])
 def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
     _lib.load().nnp_set_gemm_mode(gemm_mode)
     try:
@@ -106,7 +106,7 @@ def test_periodic_triclinic_and_lower_cutoff(rng, gemm_mode):
                             cutoff_upper=4.5, max_z=10, seed=6)
         check(model, z, pos, None, box)
     finally:
-        _lib.load().nnp_set_gemm_mode(3)
+        _lib.load().nnp_set_gemm_mode(_lib.DEFAULT_GEMM_MODE)
 
 
 def test_config_a_alanine_sized_molecule():
