@@ -857,7 +857,8 @@ static int launch_wstat(const GemmBatch &b, int count, cudaStream_t stream)
 constexpr int ST_STAGES = 7;
 constexpr int ST_LAG = 5;                           // chunks in flight behind the newest request
 constexpr int ST_PRODUCERS = 256;
-constexpr int ST_THREADS = 128 + 32 + ST_PRODUCERS;
+constexpr int ST_EPI_WARPS = 8;                     // two per TMEM lane quadrant, 64 tile rows each
+constexpr int ST_THREADS = 128 + 32 + ST_PRODUCERS + 128;
 constexpr int ST_STAGE_BYTES = 2 * BM * 128;        // raw (= hi) and lo, 128 rows x 128 B each
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes)
@@ -878,7 +879,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
     constexpr int N = 128, K = 128, NCHUNK = K / KC;
     extern __shared__ char smem_raw[];
     char *ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ uint64_t full_bar[ST_STAGES], empty_bar[ST_STAGES], tfull_bar[2], tempty_bar[2];
+    __shared__ uint64_t full_bar[ST_STAGES], empty_bar[ST_STAGES], tfull_bar[2], tempty_bar[2], w_bar;
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -896,8 +897,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 128);
+            mbar_init(&tempty_bar[a], 32 * ST_EPI_WARPS);
         }
+        mbar_init(&w_bar, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -932,12 +934,11 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
             tmem_st16(lane_addr + (uint32_t)(K + k0), lo);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&w_bar);        // only the MMA thread waits for the weights; loads start at once
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    if (warp >= 5) {
+    if (warp >= 5 && warp < 13) {
         // ============================================================ producers (256 threads)
         const int ptid = tid - 160;
         constexpr int PIECES = BM * 8 / ST_PRODUCERS;       // 16-byte pieces per thread per chunk (4)
@@ -1001,6 +1002,8 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
         if (lane == 0) {
             const uint32_t idesc = make_idesc(N);
             int it = 0, tcount = 0;
+            mbar_wait(&w_bar, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int tile = my; tile < tiles; tile += stride, ++tcount) {
                 const int acc = tcount & 1;
                 const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
@@ -1033,7 +1036,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
         // Four warps, one per scheduler, have nothing to hide latency behind, so the per-element
         // work is a pointer bump: rows of a tile are walked in order and the [node][9][C]
         // addressing (ncomp rows per node, then a skip of 9 - ncomp rows) is kept incrementally.
-        const int n = warp * 32 + lane;                     // accumulator lane = output channel
+        const int quad = warp & 3;                          // TMEM lane quadrant this warp may read
+        const int hrow = warp < 4 ? 0 : BM / 2;             // first tile row of this warp's half
+        const int n = quad * 32 + lane;                     // accumulator lane = output channel
         const int ncomp = g.ncomp;
         const int wrap = ncomp > 0 ? ncomp : 0x7fffffff;
         const int ldo = g.ldo;
@@ -1043,8 +1048,8 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
         for (int tile = my; tile < tiles; tile += stride, ++tcount) {
             const int acc = tcount & 1;
             const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
-            const int r0 = tile * BM;
-            const int rows = g.M - r0 < BM ? g.M - r0 : BM;
+            const int r0 = tile * BM + hrow;
+            const int rows = g.M - r0 < BM / 2 ? g.M - r0 : BM / 2;
             int node = node_of(ncomp, r0);
             int comp = ncomp > 0 ? r0 - node * ncomp : 0;
             const size_t prow = ncomp > 0 ? (size_t)node * 9 + g.q0 + comp : (size_t)r0;
@@ -1055,7 +1060,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
             int off = 0, goff = 0;                          // running element offsets from po / pg
             bool waited = false;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BM; c0 += 16) {
+            for (int c0 = 0; c0 < BM / 2; c0 += 16) {
                 if (c0 >= rows) break;
                 // addresses of this block's 16 rows, and every global read issued up front
                 int o[16];
@@ -1081,7 +1086,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
                     waited = true;
                 }
                 float v[16];
-                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(2 * K + acc * N + c0), v);
+                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(2 * K + acc * N + hrow + c0), v);
                 // v[i] = out[row c0 + i][channel n]: the warp's 32 lanes cover one 128-byte line per row
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -1100,6 +1105,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
                     }
                 }
             }
+            if (!waited) mbar_wait(&tfull_bar[acc], acc_ph);
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(&tempty_bar[acc]);
         }

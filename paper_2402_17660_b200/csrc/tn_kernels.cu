@@ -399,8 +399,10 @@ __device__ __forceinline__ void st9(float *base, int C, const float *c9)
     for (int q = 0; q < 9; ++q) base[(size_t)q * C] = c9[q];
 }
 
-__global__ void k_normalize(const float *__restrict__ X, float *__restrict__ Xh,
-                            float *__restrict__ nx, int n, int C)
+// Xh = X / (|X|^2 + 1); with e1 != NULL the input is the embedding's mixed tensor Xm and
+// X = Xm * silu(e1)[grp] is formed on the fly (the gated X itself is never stored)
+__global__ void k_normalize(const float *__restrict__ X, const float *__restrict__ e1,
+                            float *__restrict__ Xh, float *__restrict__ nx, int n, int C)
 {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
@@ -408,6 +410,12 @@ __global__ void k_normalize(const float *__restrict__ X, float *__restrict__ Xh,
     const size_t off = (size_t)node * 9 * C + c;
     float x[9], xh[9];
     ld9(X + off, C, x);
+    if (e1) {
+        const float *e = e1 + (size_t)node * 3 * C + 3 * c;
+        const float gate[3] = {nnp_silu(e[0]), nnp_silu(e[1]), nnp_silu(e[2])};
+#pragma unroll
+        for (int q = 0; q < 9; ++q) x[q] *= gate[group_of(q)];
+    }
     nx[idx] = normalize_fwd(x, xh);
     st9(Xh + off, C, xh);
 }
@@ -480,15 +488,20 @@ __global__ void k_node_product_bwd(const float *__restrict__ Mc, const float *__
     st9(GY + off, C, gy);
 }
 
-__global__ void k_normalize_bwd(const float *__restrict__ GXh, const float *__restrict__ Xh,
-                                const float *__restrict__ nx, float *__restrict__ GX, int n, int C)
+// dL/dXh arrives in two parts (the residual path GXa and the mixed-back edge path GXb)
+__global__ void k_normalize_bwd(const float *__restrict__ GXa, const float *__restrict__ GXb,
+                                const float *__restrict__ Xh, const float *__restrict__ nx,
+                                float *__restrict__ GX, int n, int C)
 {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
     const size_t off = (size_t)node * 9 * C + c;
-    float g[9], xh[9], gx[9];
-    ld9(GXh + off, C, g);
+    float g[9], g2[9], xh[9], gx[9];
+    ld9(GXa + off, C, g);
+    ld9(GXb + off, C, g2);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] += g2[q];
     ld9(Xh + off, C, xh);
     normalize_bwd(g, xh, nx[idx], gx);
     st9(GX + off, C, gx);
@@ -1385,14 +1398,19 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
         b.g[0] = plain_gemm(d.e0, m.es1_w, m.es1_b, d.e1, n, 3 * C, 2 * C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
-        GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xa, n, C, d.Xm, d.e1, 3 * C);
-        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st))); }
+        if (L == 0) {
+            GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xa, n, C, d.Xm, d.e1, 3 * C);
+            { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st))); }
+        } else {   // the gate is applied by the first layer's normalisation
+            GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xm, n, C);
+            { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
+        }
     }
     float *X = d.Xa, *Xother = d.Xb;
 
     // ---- interaction layers
     for (int l = 0; l < L; ++l) {
-        if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(X, d.Xh[l], d.nx[l], n, C); }
+        if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xm, d.e1, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
         static const int fwd_split = env_int("NNP_FWD_SPLIT", 1);
@@ -1440,10 +1458,10 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
         { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc))); }
-        // G_Xh = GX + mix^T(G_Y)  -> written in place over GX
-        GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GX, n, C, nullptr, GX, C);
-        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_ADD>(mh, 3, st))); }
-        { NNP_PROF("k_normalize_bwd", st); k_normalize_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Xh[l], d.nx[l], Gb, n, C); }
+        // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
+        GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
+        { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }
+        { NNP_PROF("k_normalize_bwd", st); k_normalize_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, Ga, d.Xh[l], d.nx[l], Gb, n, C); }
         std::swap(GX, Gb);
     }
 
