@@ -969,19 +969,19 @@ __global__ void k_head(TnDev d, int H)
 }
 
 // per-sample sums in float64, fixed order (graphnet.py:411 segment_sum over batch)
-__global__ void __launch_bounds__(256) k_energy_sum(TnDev d)
+__global__ void __launch_bounds__(1024) k_energy_sum(TnDev d)
 {
     const int b = blockIdx.x;
     const int p0 = d.sample_ptr[b], p1 = d.sample_ptr[b + 1];
     double acc = 0.0;
     for (int i = p0 + threadIdx.x; i < p1; i += blockDim.x) acc += (double)d.e_atom[i];
-    __shared__ double sh[8];
+    __shared__ double sh[32];
     acc = nnp_warp_sum(acc);
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += sh[w];
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
         d.energy[b] = (float)t;
     }
 }
@@ -1127,10 +1127,15 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
     const int cb = part * 32 * CPL + lane * CPL;
     float zr[CPL];
     ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
-    float G[9][CPL];
+    float G[9][CPL], g0x3[CPL], szz[CPL];
     const float *p = GX0 + (size_t)s * 9 * C + cb;
 #pragma unroll
     for (int q = 0; q < 9; ++q) ldv<CPL>(p + q * C, G[q]);
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        g0x3[v] = 3.0f * G[0][v];
+        szz[v] = -G[4][v] - G[5][v];
+    }
     const float inv_step = 1.0f / d.m.u_step;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
     for (int e = e0; e < e1; ++e) {
@@ -1142,26 +1147,32 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
         table_lookup<C, CPL, true>(d.m.tables_mono, d.m.num_knots, ga.x, cb, f, df);
-        float b[9];
-        edge_basis9(gb.x, gb.y, gb.z, b);
+        // per-edge scalars of the unit tensors: <G, b>_A = 2 (G1 ux + G2 uy + G3 uz),
+        // <G, b>_S = G4 (2 b4 + b5) + G5 (2 b5 + b4) + 2 (G6 b6 + G7 b7 + G8 b8)
+        const float uu = (gb.x * gb.x + gb.y * gb.y + gb.z * gb.z) * (1.0f / 3.0f);
+        const float b4 = gb.x * gb.x - uu, b5 = gb.y * gb.y - uu;
+        const float a1 = 2.0f * gb.x, a2 = 2.0f * gb.y, a3 = 2.0f * gb.z;
+        const float s4 = 2.0f * b4 + b5, s5 = 2.0f * b5 + b4;
+        const float s6 = a1 * gb.y, s7 = a1 * gb.z, s8 = a2 * gb.z;
         const float su = -gb.w * inv_step * ga.y;
         float pd = 0.0f, px = 0.0f, py = 0.0f, pz = 0.0f;
 #pragma unroll
         for (int v = 0; v < CPL; ++v) {
             const float Z = zr[v] + zsnd[v];
-            float g9[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) g9[q] = G[q][v];
-            const float gw0 = 3.0f * g9[0];
-            const float gw1 = 2.0f * (g9[1] * b[1] + g9[2] * b[2] + g9[3] * b[3]);
-            const float gw2 = c9_dot_S(g9, b);
-            pd += Z * (gw0 * (df[0][v] * su + f[0][v] * ga.z) + gw1 * (df[1][v] * su + f[1][v] * ga.z) +
-                       gw2 * (df[2][v] * su + f[2][v] * ga.z));
-            const float w1 = f[1][v] * ga.y * Z, w2 = f[2][v] * ga.y * Z;
-            const float szz = -g9[4] - g9[5];
-            px += 2.0f * (w1 * g9[1] + w2 * (g9[4] * gb.x + g9[6] * gb.y + g9[7] * gb.z));
-            py += 2.0f * (w1 * g9[2] + w2 * (g9[6] * gb.x + g9[5] * gb.y + g9[8] * gb.z));
-            pz += 2.0f * (w1 * g9[3] + w2 * (g9[7] * gb.x + g9[8] * gb.y + szz * gb.z));
+            const float gA = fmaf(G[1][v], a1, fmaf(G[2][v], a2, G[3][v] * a3));
+            const float gS = fmaf(G[4][v], s4, fmaf(G[5][v], s5, fmaf(G[6][v], s6, fmaf(G[7][v], s7, G[8][v] * s8))));
+            const float F0 = fmaf(df[0][v], su, f[0][v] * ga.z);
+            const float F1 = fmaf(df[1][v], su, f[1][v] * ga.z);
+            const float F2 = fmaf(df[2][v], su, f[2][v] * ga.z);
+            pd = fmaf(Z, fmaf(g0x3[v], F0, fmaf(gA, F1, gS * F2)), pd);
+            const float Zp = Z * ga.y;
+            const float w1 = f[1][v] * Zp, w2 = f[2][v] * Zp;
+            const float vx = fmaf(G[4][v], gb.x, fmaf(G[6][v], gb.y, G[7][v] * gb.z));
+            const float vy = fmaf(G[6][v], gb.x, fmaf(G[5][v], gb.y, G[8][v] * gb.z));
+            const float vz = fmaf(G[7][v], gb.x, fmaf(G[8][v], gb.y, szz[v] * gb.z));
+            px = fmaf(w1, G[1][v], fmaf(w2, vx, px));
+            py = fmaf(w1, G[2][v], fmaf(w2, vy, py));
+            pz = fmaf(w1, G[3][v], fmaf(w2, vz, pz));
         }
         pd = nnp_warp_sum(pd);
         px = nnp_warp_sum(px);
@@ -1169,7 +1180,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         pz = nnp_warp_sum(pz);
         if (lane == 0) {
             d.g_d[(size_t)part * d.capacity + e] += pd;
-            d.g_u[(size_t)part * d.capacity + e] = make_float4(px, py, pz, 0.0f);
+            d.g_u[(size_t)part * d.capacity + e] = make_float4(2.0f * px, 2.0f * py, 2.0f * pz, 0.0f);
         }
     }
 }
@@ -1432,7 +1443,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
     }
     { NNP_PROF("k_head", st); k_head<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, H); }
-    { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), 256, 0, st>>>(d); }
+    { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), (n / d.n_samples >= 2048 ? 1024 : 256), 0, st>>>(d); }
     if (d.per_atom) k_copy_per_atom<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d);
     NNP_CHECK_LAUNCH("tensornet forward");
     if (!d.forces) return NNP_OK;
@@ -1457,7 +1468,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc))); }
+        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc))); } 
         // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }

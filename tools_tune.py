@@ -32,6 +32,6 @@ for _ in range(20):
     model.replay(plan)
 e.record(); torch.cuda.synchronize()
 env = {k: v for k, v in os.environ.items() if k.startswith("NNP_")}
-top = sorted(acc.items(), key=lambda kv: -kv[1])[:9]
+top = sorted(acc.items(), key=lambda kv: -kv[1])[:40]
 print(json.dumps({"env": env, "wl": wl, "graph_ms": round(s.elapsed_time(e) / 20, 4),
                   "top": {k: round(v, 4) for k, v in top}, "E": float(plan.energy[0])}))
