@@ -783,6 +783,7 @@ __global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
 // g_d[e] + g_d[reverse(e)], which is symmetric, so storing the reverse edge's term in slot e is
 // equivalent and needs no second gather (G_M[b] is already in registers, Yc[a] is the own node).
 // Two edges are processed per iteration (loads of both in flight, one shared warp reduction).
+// (launched with 128 threads: at 168 registers three blocks = 12 warps stay resident per SM)
 template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
                                                           float *GY)
@@ -1138,13 +1139,27 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
     }
     const float inv_step = 1.0f / d.m.u_step;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    // next edge's scalars are fetched one iteration ahead (their latency was the top stall)
+    int nj = 0, nz = 0;
+    float4 nga = make_float4(0.f, 0.f, 0.f, 0.f), ngb = nga;
+    if (e0 < e1) {
+        nj = d.col[e0];
+        nz = d.zs[nj];
+        nga = d.geoA[e0];
+        ngb = d.geoB[e0];
+    }
     for (int e = e0; e < e1; ++e) {
-        const int j = d.col[e];
+        const int j = nj, zj = nz;
+        const float4 ga = nga, gb = ngb;
+        if (e + 1 < e1) {
+            nj = d.col[e + 1];
+            nz = d.zs[nj];
+            nga = d.geoA[e + 1];
+            ngb = d.geoB[e + 1];
+        }
         if (j == s) continue;  // a self loop has no geometry
-        const float4 ga = d.geoA[e];
-        const float4 gb = d.geoB[e];
         float zsnd[CPL];
-        ldv<CPL>(d.m.z_send + (size_t)d.zs[j] * C + cb, zsnd);
+        ldv<CPL>(d.m.z_send + (size_t)zj * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
         table_lookup<C, CPL, true>(d.m.tables_mono, d.m.num_knots, ga.x, cb, f, df);
         // per-edge scalars of the unit tensors: <G, b>_A = 2 (G1 ux + G2 uy + G3 uz),
@@ -1338,7 +1353,7 @@ GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n,
 // node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
 // through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
 struct EdgeTuning {
-    int emb, fwd, bwd, embbwd, bwd_block, fwd_block;
+    int emb, fwd, bwd, embbwd, bwd_block, fwd_block, emb_block;
 };
 static int env_int(const char *name, int fallback)
 {
@@ -1347,9 +1362,9 @@ static int env_int(const char *name, int fallback)
 }
 static const EdgeTuning &edge_tuning()
 {
-    static const EdgeTuning t = {env_int("NNP_CPL_EMB", 2), env_int("NNP_CPL_FWD", 4),
+    static const EdgeTuning t = {env_int("NNP_CPL_EMB", 4), env_int("NNP_CPL_FWD", 4),
                                  env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
-                                 env_int("NNP_BWD_BLOCK", 128), env_int("NNP_FWD_BLOCK", 128)};
+                                 std::min(env_int("NNP_BWD_BLOCK", 128), 128), env_int("NNP_FWD_BLOCK", 128), env_int("NNP_EMB_BLOCK", 128)};
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -1401,7 +1416,7 @@ int run_step(TnDev &d, cudaStream_t st)
     { NNP_PROF("k_edge_rev", st); k_edge_rev<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
 
     // ---- embedding
-    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d))); }
+    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d))); }
     { NNP_PROF("k_embed_ln", st); k_embed_ln<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     {
         GemmBatch b{};
@@ -1488,7 +1503,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
     { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
-    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 8)), 256, 0, st>>>(d, Gb))); }
+    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d, Gb))); }
     { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(nnp_blocks(n, 128)), 128, 0, st>>>(d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
