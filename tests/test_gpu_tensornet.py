@@ -142,6 +142,32 @@ def test_batched_molecules():
     assert torch.allclose(f_all[: int(sel.sum())], f_sub, rtol=1e-5, atol=1e-7)
 
 
+def test_lattice_ties_long_rows_and_isolated_atom():
+    """Rows far longer than a warp, many exactly equal distances (the in-row ordering by table
+    coordinate must break ties consistently), an atom whose only edge is its self loop, and the
+    capacity growth that a 200-neighbour row forces."""
+    g = np.arange(5) * 1.3
+    pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    pos = np.concatenate([pos, [[40.0, 40.0, 40.0]]]).astype(np.float32).astype(np.float64)
+    z = np.resize([1, 6, 8], len(pos))
+    for C, L in ((32, 2), (128, 1)):
+        model = P.TensorNet(embedding_dimension=C, num_layers=L, num_rbf=16, cutoff_upper=5.0,
+                            max_z=10, seed=9)
+        check(model, z, pos, None, None)
+
+
+def test_three_layer_triclinic_config_e_shape():
+    """Config E's shape at a size the oracle finishes quickly: triclinic box, 3 layers."""
+    L = 24.0
+    box = np.array([[L, 0, 0], [0.3 * L, L, 0], [0.2 * L, -0.25 * L, L]])
+    rng = np.random.default_rng(5)
+    pos = (rng.uniform(0, 1, (700, 3)) @ box).astype(np.float32).astype(np.float64)
+    z = rng.choice([1, 8], 700, p=[2 / 3, 1 / 3])
+    model = P.TensorNet(embedding_dimension=64, num_layers=3, num_rbf=32, cutoff_upper=5.0,
+                        max_z=10, seed=4, strategy="cell")
+    check(model, z, pos, None, box)
+
+
 def test_graph_replay_equals_eager_and_is_deterministic(rng):
     z, pos, batch, _ = small_open(rng, 30)
     args = (torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
