@@ -113,12 +113,11 @@ int nnp_distance_pullback(const int32_t *pairs, const double *deltas, const doub
  */
 #define NNP_TN_MAX_LAYERS 8
 
-/* A GEMM weight W[N,K] (row-major float32) plus, for the tcgen05 path, its TF32 hi/lo split
- * pre-arranged as shared-memory tile images: [N/NT][ceil(K/32)][NT rows][32 floats], each row's
- * eight 16-byte chunks XOR-swizzled by (row % 8) (the K-major SWIZZLE_128B operand layout), NT =
- * 128/64/32/16 = the largest of these dividing N.  hi/lo may be NULL (slower generic path). */
-typedef struct nnp_gemm_weight {
-    const float *w, *hi, *lo;
+/* A GEMM weight W[N,K] (row-major float32 on the device).  The tensor-core kernels split it into
+ * TF32 hi/lo parts themselves (once per CTA for the 128 x 128 channel mixes, whose weight lives in
+ * tensor memory). */
+typedef struct {
+    const float *w;
 } nnp_gemm_weight;
 
 typedef struct nnp_tn_model {
@@ -183,8 +182,8 @@ int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_sampl
  * kernels use (3xTF32 tensor-core path or FP32 FFMA). */
 int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const float *bias, float *out,
                      int32_t M, int32_t N, int32_t K, nnp_stream_t stream);
-/* Test hook: 3 = tcgen05 3xTF32, one tile per CTA (default), 2 = persistent warp-specialised
- * tcgen05, 1 = mma.sync 3xTF32, 0 = FP32 FFMA inner loop. */
+/* Test hook: 5 = streaming tcgen05 3xTF32 kernel for the 128 x 128 channel mixes, other shapes as 3
+ * (default), 3 = tcgen05 3xTF32 with one tile per CTA, 1 = mma.sync 3xTF32, 0 = FP32 FFMA. */
 int nnp_set_gemm_mode(int use_mma);
 
 /* Instrumentation (bench.py / tests): number of kernels this library has enqueued so far

@@ -11,7 +11,7 @@ from .neighbors import (
     NeighborList, NeighborSpec, as_full_list, as_half_list, build_neighbor_list,
     build_with_auto_capacity, canonicalize, capacity_heuristic, distance_pullback,
 )
-from .tensornet import TNConfig, TensorNet, build_radial_tables, init_params, stage_gemm_weight
+from .tensornet import TNConfig, TensorNet, build_radial_tables, init_params
 from .compose import ComposedPotential, evaluate, evaluate_auto
 
 __version__ = "0.1.0"

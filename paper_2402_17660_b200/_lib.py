@@ -45,7 +45,7 @@ class NlParams(ctypes.Structure):
 
 
 class GemmWeight(ctypes.Structure):
-    _fields_ = [("w", _p), ("hi", _p), ("lo", _p)]
+    _fields_ = [("w", _p)]
 
 
 class TnModel(ctypes.Structure):

@@ -20,7 +20,6 @@ enum { EPI_STORE = 0, EPI_MUL_SILU_GRAD = 1, EPI_GATE = 2, EPI_ADD = 3 };
 struct GemmArgs {
     const float *A;
     const float *W;
-    const float *Whi, *Wlo;  // TF32 hi/lo tile images of W (tensornet.stage_gemm_weight) or NULL
     const float *bias;
     float *out;
     float *out2;

@@ -277,298 +277,12 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
 }
 
 
-// ------------------------------------------------------------------------------------------
-// Persistent, warp-specialised version (the one the model step uses).  One CTA per SM loops over
-// output tiles; three roles run concurrently and meet only through mbarriers:
-//   warps 4-7  producers : A rows global -> registers -> TF32 hi/lo split -> swizzled smem stage
-//   warp  8    (1 thread): bulk-copies (cp.async.bulk, complete_tx on the stage's "full" barrier)
-//                          the pre-split, pre-swizzled weight chunk images, then issues the
-//                          tcgen05.mma triple per K step and commits to "empty" / "tmem_full"
-//   warps 0-3  epilogue  : tcgen05.ld of the finished accumulator -> swizzled smem staging tile ->
-//                          coalesced float4 global stores with the fused epilogue
-// Two operand stages and two TMEM accumulators let the loads of chunk c+1, the MMAs of chunk c
-// and the epilogue of the previous tile overlap.  Weights are split/swizzled once on the host
-// (tensornet.stage_gemm_weight), so the per-tile producer work is the activation tile only.
-constexpr int WS_THREADS = 288;
-constexpr int WS_STAGES = 2;
-
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst_smem)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-struct TileCoord {
-    int z, m0, nt_idx;
-};
-
-__device__ __forceinline__ bool decode_tile(const GemmBatch &b, int count, int n_tiles_n, int tile,
-                                            TileCoord &tc)
-{
-    for (int z = 0; z < count; ++z) {
-        const int tm = (b.g[z].M + BM - 1) / BM;
-        const int tz = tm * n_tiles_n;
-        if (tile < tz) {
-            tc.z = z;
-            tc.m0 = (tile / n_tiles_n) * BM;
-            tc.nt_idx = tile % n_tiles_n;
-            return true;
-        }
-        tile -= tz;
-    }
-    return false;
-}
-
-template <int PRO, int EPI, int NT>
-__global__ void __launch_bounds__(WS_THREADS, 1) gemm_tc5_ws_kernel(GemmBatch batch, int count,
-                                                                   int total_tiles, int n_tiles_n)
-{
-    constexpr int TMEM_COLS = (2 * NT) <= 32 ? 32 : ((2 * NT) <= 64 ? 64 : ((2 * NT) <= 128 ? 128 : 256));
-    constexpr int A_PASSES = BM / 16;
-    constexpr int STAGE_BYTES = 2 * BM * 128 + 2 * NT * 128;
-    constexpr int CH = NT / 4;
-
-    extern __shared__ char smem_raw[];
-    char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space
-    float *stage_out = reinterpret_cast<float *>(smem + WS_STAGES * STAGE_BYTES);
-    __shared__ uint64_t full_bar[WS_STAGES], empty_bar[WS_STAGES], tfull_bar[2], tempty_bar[2];
-    __shared__ uint32_t tmem_base_s;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < WS_STAGES; ++s) {
-            mbar_init(&full_bar[s], 128 + 1);   // 128 producer threads + the expect_tx arrival
-            mbar_init(&empty_bar[s], 1);        // tcgen05.commit
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull_bar[a], 1);        // tcgen05.commit
-            mbar_init(&tempty_bar[a], 128);     // epilogue threads
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&tmem_base_s)),
-                     "n"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem_base = tmem_base_s;
-
-    if (warp >= 4 && warp < 8) {
-        // ===================================================================== producers
-        const int ptid = tid - 128;
-        const int lrow = ptid >> 3, lchunk = ptid & 7;
-        int it = 0;   // running chunk counter -> stage and phase
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            TileCoord tc;
-            decode_tile(batch, count, n_tiles_n, tile, tc);
-            const GemmArgs &g = batch.g[tc.z];
-            const int nchunks = (g.K + KC - 1) / KC;
-            const float *a_ptr[A_PASSES];
-#pragma unroll
-            for (int p = 0; p < A_PASSES; ++p) {
-                const int r = tc.m0 + p * 16 + lrow;
-                a_ptr[p] = r < g.M ? g.A + (size_t)gemm_phys_row(g, r) * g.lda + lchunk * 4 : nullptr;
-            }
-            float4 ra[A_PASSES];
-            auto load_chunk = [&](int c) {
-                const int k0 = c * KC;
-                const bool k_ok = k0 + lchunk * 4 < g.K;
-#pragma unroll
-                for (int p = 0; p < A_PASSES; ++p) {
-                    ra[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (a_ptr[p] && k_ok) ra[p] = __ldg(reinterpret_cast<const float4 *>(a_ptr[p] + k0));
-                }
-            };
-            load_chunk(0);
-            for (int c = 0; c < nchunks; ++c, ++it) {
-                const int s = it % WS_STAGES;
-                const uint32_t ph = (uint32_t)((it / WS_STAGES) & 1);
-                mbar_wait(&empty_bar[s], ph ^ 1);          // stage free (passes at once the first time)
-                char *a_hi = smem + s * STAGE_BYTES, *a_lo = a_hi + BM * 128;
-#pragma unroll
-                for (int p = 0; p < A_PASSES; ++p) {
-                    float4 v = ra[p];
-                    if (PRO == PRO_SILU) {
-                        v.x = nnp_silu(v.x);
-                        v.y = nnp_silu(v.y);
-                        v.z = nnp_silu(v.z);
-                        v.w = nnp_silu(v.w);
-                    }
-                    split_store(a_hi, a_lo, swz(p * 16 + lrow, lchunk), v);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(&full_bar[s]);
-                if (c + 1 < nchunks) load_chunk(c + 1);
-            }
-        }
-    } else if (warp == 8) {
-        // ===================================================== weight copies + MMA issue (1 thread)
-        if (lane == 0) {
-            const uint32_t idesc = make_idesc(NT);
-            int it = 0, tcount = 0;
-            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++tcount) {
-                TileCoord tc;
-                decode_tile(batch, count, n_tiles_n, tile, tc);
-                const GemmArgs &g = batch.g[tc.z];
-                const int nchunks = (g.K + KC - 1) / KC;
-                const int acc = tcount & 1;
-                const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
-                mbar_wait(&tempty_bar[acc], acc_ph ^ 1);   // epilogue has drained this accumulator
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t tmem_d = tmem_base + (uint32_t)(acc * NT);
-                for (int c = 0; c < nchunks; ++c, ++it) {
-                    const int s = it % WS_STAGES;
-                    const uint32_t ph = (uint32_t)((it / WS_STAGES) & 1);
-                    char *a_hi = smem + s * STAGE_BYTES, *a_lo = a_hi + BM * 128;
-                    char *w_hi = a_hi + 2 * BM * 128, *w_lo = w_hi + NT * 128;
-                    mbar_wait(&empty_bar[s], ph ^ 1);
-                    const size_t woff = ((size_t)tc.nt_idx * nchunks + c) * (size_t)(NT * 32);
-                    mbar_expect_tx(&full_bar[s], 2u * NT * 128u);
-                    bulk_g2s(w_hi, g.Whi + woff, NT * 128u, &full_bar[s]);
-                    bulk_g2s(w_lo, g.Wlo + woff, NT * 128u, &full_bar[s]);
-                    mbar_wait(&full_bar[s], ph);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint64_t da_hi = make_desc(smem_u32(a_hi)), da_lo = make_desc(smem_u32(a_lo));
-                    const uint64_t dw_hi = make_desc(smem_u32(w_hi)), dw_lo = make_desc(smem_u32(w_lo));
-#pragma unroll
-                    for (int ks = 0; ks < KC / 8; ++ks) {
-                        const uint64_t adv = (uint64_t)(ks * 32 >> 4);
-                        umma_tf32(tmem_d, da_lo + adv, dw_hi + adv, idesc, (c | ks) != 0);
-                        umma_tf32(tmem_d, da_hi + adv, dw_lo + adv, idesc, 1);
-                        umma_tf32(tmem_d, da_hi + adv, dw_hi + adv, idesc, 1);
-                    }
-                    umma_commit(&empty_bar[s]);                   // stage reusable when these MMAs retire
-                    if (c + 1 == nchunks) umma_commit(&tfull_bar[acc]);
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp < 4) {
-        // ====================================================================== epilogue
-        int tcount = 0;
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++tcount) {
-            TileCoord tc;
-            decode_tile(batch, count, n_tiles_n, tile, tc);
-            const GemmArgs &g = batch.g[tc.z];
-            const int acc = tcount & 1;
-            const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
-            mbar_wait(&tfull_bar[acc], acc_ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int rr = warp * 32 + lane;
-#pragma unroll 1
-            for (int c0 = 0; c0 < NT; c0 += 16) {
-                float v[16];
-                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * NT + c0), v);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int pos = ((c0 >> 2) + q) ^ (rr & (CH - 1));
-                    *reinterpret_cast<float4 *>(stage_out + rr * NT + pos * 4) =
-                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&tempty_bar[acc]);                       // accumulator may be overwritten
-            asm volatile("bar.sync 1, 128;" ::: "memory");       // staging tile complete
-            constexpr int ROWS_PER_IT = 32 / CH;
-            const int n0 = tc.nt_idx * NT;
-            for (int r0 = warp * ROWS_PER_IT; r0 < BM; r0 += 4 * ROWS_PER_IT) {
-                const int row = r0 + lane / CH;
-                const int ch = lane % CH;
-                const int pos = ch ^ (row & (CH - 1));
-                const float4 v = *reinterpret_cast<const float4 *>(stage_out + row * NT + pos * 4);
-                gemm_epilogue4<EPI>(g, tc.m0 + row, n0 + ch * 4, v);
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");       // staging tile free again
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS)
-                     : "memory");
-    }
-}
-
-template <int PRO, int EPI, int NT>
-static int launch_ws_nt(const GemmBatch &b, int count, int maxN, cudaStream_t stream)
-{
-    constexpr int smem = WS_STAGES * (2 * BM * 128 + 2 * NT * 128) + BM * NT * 4 + 1024;
-    static int num_sms = 0;
-    if (num_sms == 0) {
-        cudaFuncSetAttribute(gemm_tc5_ws_kernel<PRO, EPI, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
-    const int n_tiles_n = maxN / NT;
-    int total = 0;
-    for (int i = 0; i < count; ++i) total += ((b.g[i].M + BM - 1) / BM) * n_tiles_n;
-    if (total <= 0) return NNP_OK;
-    const int grid = total < num_sms ? total : num_sms;
-    gemm_tc5_ws_kernel<PRO, EPI, NT><<<NNP_GRID(grid), WS_THREADS, smem, stream>>>(b, count, total, n_tiles_n);
-    NNP_CHECK_LAUNCH("gemm_tc5_ws");
-    return NNP_OK;
-}
-
-// NT the host staged the weight images for (must match tensornet.gemm_tile_n)
-static inline int tile_n_for(int N) { return N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : (N % 32 == 0 ? 32 : 16)); }
-
-template <int PRO, int EPI>
-static int launch_ws(const GemmBatch &b, int count, cudaStream_t stream)
-{
-    const int N = b.g[0].N;
-    for (int i = 0; i < count; ++i)
-        if (b.g[i].N != N || !b.g[i].Whi || !b.g[i].Wlo || N % 16 != 0) return -100;
-    switch (tile_n_for(N)) {
-    case 128: return launch_ws_nt<PRO, EPI, 128>(b, count, N, stream);
-    case 64: return launch_ws_nt<PRO, EPI, 64>(b, count, N, stream);
-    case 32: return launch_ws_nt<PRO, EPI, 32>(b, count, N, stream);
-    default: return launch_ws_nt<PRO, EPI, 16>(b, count, N, stream);
-    }
-}
-
-
-// ------------------------------------------------------------------------------------------
-// Weight-stationary kernel for the channel-mixing GEMMs (N = K = 128): the model's hot GEMM shape.
-//
-//   out^T[n, r] = sum_k W[n, k] * X[r, k]
-//
-// The roles of the operands are swapped with respect to the kernels above: the 128 x 128 weight
-// matrix is the MMA's A operand and lives in TENSOR MEMORY for the whole life of the CTA (TF32
-// hi part in columns [0,128), lo part in [128,256); lane = output channel), written once with
-// tcgen05.st.  The activation rows stream through shared memory as the B operand (K-major
-// SWIZZLE_128B, hi/lo split on the fly by 8 producer warps, 4 stages deep, loads issued two
-// chunks ahead), and two 128-column accumulators ([256,384) and [384,512)) let the epilogue of one
-// row tile overlap the MMAs of the next.  With the weights out of shared memory the whole 227 KB
-// goes to activation staging, which is what it takes to keep enough HBM requests in flight.
-// CTAs are persistent and bound to one component group (one weight matrix); the three groups get
-// CTAs in proportion to their row counts.
-constexpr int WST_STAGES = 4;
-constexpr int WST_PRODUCERS = 256;
-constexpr int WST_THREADS = 128 + WST_PRODUCERS + 32;
-constexpr int WST_STAGE_BYTES = 2 * BM * 128;   // 128 rows x 128 B, hi and lo
-
+// tcgen05.mma with the A operand in tensor memory
 __device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
                                              uint32_t accumulate)
 {
@@ -590,250 +304,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         : "memory");
 }
 
-struct WstatSchedule {
+struct StreamSchedule {
     int cta_begin[4];   // CTAs [cta_begin[z], cta_begin[z+1]) serve problem z
 };
-
-template <int PRO, int EPI>
-__global__ void __launch_bounds__(WST_THREADS, 1) gemm_wstat_kernel(GemmBatch batch, WstatSchedule sched)
-{
-    constexpr int N = 128, K = 128, NCHUNK = K / KC;
-    extern __shared__ char smem_raw[];
-    char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space
-    float *stage_out = reinterpret_cast<float *>(smem + WST_STAGES * WST_STAGE_BYTES);
-    __shared__ uint64_t full_bar[WST_STAGES], empty_bar[WST_STAGES], tfull_bar[2], tempty_bar[2];
-    __shared__ uint32_t tmem_base_s;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    int z = 0;
-    while (z < 2 && (int)blockIdx.x >= sched.cta_begin[z + 1]) ++z;
-    const int my = blockIdx.x - sched.cta_begin[z];
-    const int stride = sched.cta_begin[z + 1] - sched.cta_begin[z];
-    const GemmArgs &g = batch.g[z];
-    const int tiles = (g.M + BM - 1) / BM;
-
-    if (tid == 0) {
-        for (int s = 0; s < WST_STAGES; ++s) {
-            mbar_init(&full_bar[s], WST_PRODUCERS);
-            mbar_init(&empty_bar[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&tmem_base_s)),
-                     "n"(512)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem_base = tmem_base_s;
-
-    // weights -> tensor memory (once): lane = output channel n, column k (hi) / 128 + k (lo)
-    if (warp < 4) {
-        const int n = warp * 32 + lane;
-        const float *wrow = g.W + (size_t)n * K;
-        const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int k0 = 0; k0 < K; k0 += 16) {
-            uint32_t hi[16], lo[16];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(wrow + k0 + 4 * q));
-                tf32_split(v.x, hi[4 * q], lo[4 * q]);
-                tf32_split(v.y, hi[4 * q + 1], lo[4 * q + 1]);
-                tf32_split(v.z, hi[4 * q + 2], lo[4 * q + 2]);
-                tf32_split(v.w, hi[4 * q + 3], lo[4 * q + 3]);
-            }
-            tmem_st16(lane_addr + (uint32_t)k0, hi);
-            tmem_st16(lane_addr + (uint32_t)(K + k0), lo);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-    if (warp >= 4 && warp < 12) {
-        // ============================================================ producers (256 threads)
-        const int ptid = tid - 128;
-        const int lrow = ptid >> 3, lchunk = ptid & 7;      // 32 rows x 8 chunks per pass, 4 passes
-        constexpr int PASSES = BM / 32;
-        const int total = ((tiles - my + stride - 1) / stride) * NCHUNK;   // chunks this CTA produces
-        float4 buf[2][PASSES];
-        auto issue = [&](int it, float4 (&dst)[PASSES]) {
-            const int tile = my + (it / NCHUNK) * stride;
-            const int k0 = (it % NCHUNK) * KC + lchunk * 4;
-#pragma unroll
-            for (int p = 0; p < PASSES; ++p) {
-                const int r = tile * BM + p * 32 + lrow;
-                dst[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (r < g.M && !(g.dbg & 1))
-                    dst[p] = __ldg(reinterpret_cast<const float4 *>(g.A + (size_t)gemm_phys_row(g, r) * g.lda + k0));
-            }
-        };
-        auto produce = [&](int it, float4 (&cur)[PASSES]) {
-            const int s = it % WST_STAGES;
-            const uint32_t ph = (uint32_t)((it / WST_STAGES) & 1);
-            mbar_wait(&empty_bar[s], ph ^ 1);
-            char *x_hi = smem + s * WST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
-            if (!(g.dbg & 32)) {
-#pragma unroll
-                for (int p = 0; p < PASSES; ++p) {
-                    float4 v = cur[p];
-                    if (PRO == PRO_SILU) {
-                        v.x = nnp_silu(v.x);
-                        v.y = nnp_silu(v.y);
-                        v.z = nnp_silu(v.z);
-                        v.w = nnp_silu(v.w);
-                    }
-                    split_store(x_hi, x_lo, swz(p * 32 + lrow, lchunk), v);
-                }
-            }
-            if (!(g.dbg & 8)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&full_bar[s]);
-            if (it + 2 < total) issue(it + 2, cur);             // two chunks ahead
-        };
-        if (total > 0) issue(0, buf[0]);
-        if (total > 1) issue(1, buf[1]);
-        for (int it = 0; it < total; it += 2) {                 // ping-pong with static buffers
-            produce(it, buf[0]);
-            if (it + 1 < total) produce(it + 1, buf[1]);
-        }
-    } else if (warp == 12) {
-        // ================================================================ MMA issue (1 thread)
-        if (lane == 0) {
-            const uint32_t idesc = make_idesc(N);
-            int it = 0, tcount = 0;
-            for (int tile = my; tile < tiles; tile += stride, ++tcount) {
-                const int acc = tcount & 1;
-                const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
-                mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t tmem_d = tmem_base + (uint32_t)(2 * K + acc * N);
-                for (int c = 0; c < NCHUNK; ++c, ++it) {
-                    const int s = it % WST_STAGES;
-                    const uint32_t ph = (uint32_t)((it / WST_STAGES) & 1);
-                    char *x_hi = smem + s * WST_STAGE_BYTES, *x_lo = x_hi + BM * 128;
-                    mbar_wait(&full_bar[s], ph);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint64_t dx_hi = make_desc(smem_u32(x_hi)), dx_lo = make_desc(smem_u32(x_lo));
-#pragma unroll
-                    for (int ks = 0; ks < KC / 8; ++ks) {
-                        if (g.dbg & 2) break;
-                        const uint64_t adv = (uint64_t)(ks * 32 >> 4);
-                        const uint32_t kcol = (uint32_t)(c * KC + ks * 8);
-                        umma_tf32_ta(tmem_d, tmem_base + K + kcol, dx_hi + adv, idesc, (c | ks) != 0);  // W_lo * X_hi
-                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_lo + adv, idesc, 1);                  // W_hi * X_lo
-                        umma_tf32_ta(tmem_d, tmem_base + kcol, dx_hi + adv, idesc, 1);                  // W_hi * X_hi
-                    }
-                    umma_commit(&empty_bar[s]);
-                    if (c + 1 == NCHUNK) umma_commit(&tfull_bar[acc]);
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp < 4) {
-        // ==================================================================== epilogue
-        int tcount = 0;
-        const int n = warp * 32 + lane;                     // this thread's accumulator lane = channel
-        for (int tile = my; tile < tiles; tile += stride, ++tcount) {
-            const int acc = tcount & 1;
-            const uint32_t acc_ph = (uint32_t)((tcount >> 1) & 1);
-            mbar_wait(&tfull_bar[acc], acc_ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 16) {
-                if (g.dbg & 16) break;
-                float v[16];
-                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(2 * K + acc * N + c0), v);
-                // v[i] = out[row c0 + i][channel n]: transpose through the [row][channel] staging tile
-#pragma unroll
-                for (int i = 0; i < 16; ++i) stage_out[(c0 + i) * N + n] = v[i];
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&tempty_bar[acc]);
-            if (EPI == EPI_STORE && g.bias == nullptr && !(g.dbg & 512)) {
-                // plain store: hand the staged rows to the bulk-copy engine (one 512-byte
-                // cp.async.bulk per output row, issued by one lane per warp), no per-lane traffic
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (lane == 0) {
-                    for (int row = warp; row < BM; row += 4) {
-                        const int r = tile * BM + row;
-                        if (r < g.M) {
-                            float *dst = g.out + (size_t)gemm_phys_row(g, r) * g.ldo;
-                            asm volatile(
-                                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                                "r"(smem_u32(stage_out + row * N)), "r"(N * 4)
-                                : "memory");
-                        }
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging readable again
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            } else {
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll 4
-                for (int row = warp; row < BM; row += 4) {
-                    const float4 v = *reinterpret_cast<const float4 *>(stage_out + row * N + lane * 4);
-                    if (!(g.dbg & 4)) gemm_epilogue4<EPI>(g, tile * BM + row, lane * 4, v);
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512)
-                     : "memory");
-    }
-}
-
-template <int PRO, int EPI>
-static int launch_wstat(const GemmBatch &b, int count, cudaStream_t stream)
-{
-    if (count < 1 || count > 3) return -100;
-    for (int i = 0; i < count; ++i)
-        if (b.g[i].N != 128 || b.g[i].K != 128 || b.g[i].lda % 4 != 0) return -100;
-    constexpr int smem = WST_STAGES * WST_STAGE_BYTES + BM * 128 * 4 + 1024;
-    static int num_sms = 0;
-    if (num_sms == 0) {
-        cudaFuncSetAttribute(gemm_wstat_kernel<PRO, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
-    // CTAs per problem in proportion to its tiles (at least one, at most one per tile)
-    int tiles[3] = {0, 0, 0}, total = 0;
-    for (int i = 0; i < count; ++i) {
-        tiles[i] = (b.g[i].M + BM - 1) / BM;
-        total += tiles[i];
-    }
-    if (total <= 0) return NNP_OK;
-    WstatSchedule sc{};
-    int used = 0;
-    for (int i = 0; i < count; ++i) {
-        int c = (int)(((int64_t)tiles[i] * num_sms + total - 1) / total);
-        c = std::max(1, std::min(c, tiles[i]));
-        if (tiles[i] == 0) c = 0;
-        sc.cta_begin[i] = used;
-        used += c;
-    }
-    for (int i = count; i < 4; ++i) sc.cta_begin[i] = used;
-    gemm_wstat_kernel<PRO, EPI><<<NNP_GRID(used), WST_THREADS, smem, stream>>>(b, sc);
-    NNP_CHECK_LAUNCH("gemm_wstat");
-    return NNP_OK;
-}
 
 // ------------------------------------------------------------------------------------------
 // Streaming kernel for the channel-mixing GEMMs (N = K = 128), mode 5: the one the step uses.
@@ -874,7 +347,7 @@ __device__ __forceinline__ void cp_async_wait()
 }
 
 template <int PRO, int EPI>
-__global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch batch, WstatSchedule sched)
+__global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch batch, StreamSchedule sched)
 {
     constexpr int N = 128, K = 128, NCHUNK = K / KC;
     extern __shared__ char smem_raw[];
@@ -1143,7 +616,7 @@ static int launch_stream(const GemmBatch &b, int count, cudaStream_t stream)
     }
     if (total <= 0) return NNP_OK;
     // CTAs per problem in proportion to its tiles (at least one, at most one per tile)
-    WstatSchedule sc{};
+    StreamSchedule sc{};
     int used = 0;
     for (int i = 0; i < count; ++i) {
         int c = (int)(((int64_t)tiles[i] * num_sms) / total);
@@ -1214,11 +687,12 @@ static int gemm_launch(const GemmBatch &b_in, int count, cudaStream_t stream)
         }
     }
     if (maxM <= 0) return NNP_OK;
-    if (g_nnp_gemm_use_mma >= 2) {
+    // a handful of row tiles (single small molecules) is pure launch latency: the mma.sync tile has
+    // no TMEM allocation or weight staging to pay for (measured on the 22-atom config)
+    const bool tiny = g_nnp_gemm_use_mma == 5 && maxM <= 1024;
+    if (g_nnp_gemm_use_mma >= 2 && !tiny) {
         int rc = -100;
         if (g_nnp_gemm_use_mma == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);
-        if (g_nnp_gemm_use_mma == 4) rc = tc5::launch_wstat<PRO, EPI>(b, count, stream);
-        if (g_nnp_gemm_use_mma == 2) rc = tc5::launch_ws<PRO, EPI>(b, count, stream);
         if (rc == -100) rc = tc5::launch<PRO, EPI>(b, count, stream);
         if (rc != -100) return rc;
     }

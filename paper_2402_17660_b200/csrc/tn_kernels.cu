@@ -22,8 +22,8 @@
 #include "tn_gemm_tc5.cuh"
 #include "tn_math.cuh"
 
-int g_nnp_gemm_use_mma = 5;  // 5 = streaming tcgen05 for the 128x128 mixes (default; other shapes use 3), 4 = W in TMEM,
-                              // 3 = tcgen05 one tile per CTA, 2 = persistent tcgen05, 1 = mma.sync, 0 = FFMA
+int g_nnp_gemm_use_mma = 5;  // 5 = streaming tcgen05 for the 128x128 mixes (default; other shapes use 3),
+                              // 3 = tcgen05 one tile per CTA, 1 = mma.sync, 0 = FFMA
 
 namespace {
 
@@ -65,8 +65,6 @@ constexpr int NNP_PARTS = 4;  // max channel parts a node's row is split over (C
 struct TnDev {
     nnp_tn_model m;
     int n, n_samples, capacity;
-    int dbg_nosort;  // measurement only: keep the caller's (sender-sorted) order inside rows
-    int dbg_col;  // measurement only: gather the own row instead of the sender's
     int nparts;  // channel-part slots of g_d / g_u in use this step (<= NNP_PARTS)
     // inputs
     const int *species, *batch, *order, *row_ptr, *pairs, *nl_counts;
@@ -127,7 +125,6 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
             const float db = __ldg(d.dists + b);
             rank += (db > dist || (db == dist && b < e)) ? 1 : 0;
         }
-        if (d.dbg_nosort) rank = e - e0;
         const int p = e0 + rank;
         const int i = d.pairs[2 * (size_t)e], j = d.pairs[2 * (size_t)e + 1];
         const bool loop = (i == j);
@@ -148,7 +145,7 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
         tx = fminf(fmaxf(tx, 0.0f), (float)(d.m.num_knots - 1));
         const float invd = loop ? 0.0f : 1.0f / dist;
         d.newpos[e] = p;
-        d.col[p] = d.dbg_col ? i : j;
+        d.col[p] = j;
         d.geoA[p] = make_float4(tx, phi, dphi, invd);
         d.geoB[p] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
                                 d.deltas[3 * (size_t)e + 2] * invd, u);
@@ -175,84 +172,16 @@ __global__ void k_edge_rev(TnDev d)
     d.rev[d.newpos[e]] = d.newpos[lo];
 }
 
-// Radial tables: per knot the values and (knot-spacing-scaled) slopes of the 3 radial functions,
-// [knot][value|slope][3][C].  A row walker keeps the two knots of its current interval in
-// registers; rows are sorted by table coordinate, so moving on means "same interval" (no load),
-// "next interval" (one knot) or a jump (two knots) - a warp-uniform decision.
-template <int C, int CPL>
-struct KnotCache {
-    float v0[3][CPL], m0[3][CPL], v1[3][CPL], m1[3][CPL];
-    int kn;
-
-    __device__ __forceinline__ void init() { kn = -4; }
-
-    __device__ __forceinline__ static void load_knot(const float *__restrict__ tab, int knot, int cb,
-                                                     float (&v)[3][CPL], float (&m)[3][CPL])
-    {
-        const float *row = tab + (size_t)knot * (6 * C) + cb;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            ldv<CPL>(row + k * C, v[k]);
-            ldv<CPL>(row + (3 + k) * C, m[k]);
-        }
-    }
-
-    __device__ __forceinline__ void seek(const float *__restrict__ tab, int k, int cb)
-    {
-        if (k == kn) return;
-        if (k == kn + 1) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-#pragma unroll
-                for (int v = 0; v < CPL; ++v) {
-                    v0[q][v] = v1[q][v];
-                    m0[q][v] = m1[q][v];
-                }
-        } else {
-            load_knot(tab, k, cb, v0, m0);
-        }
-        load_knot(tab, k + 1, cb, v1, m1);
-        kn = k;
-    }
-
-    // value of radial function k at t in [0,1) of the current interval
-    __device__ __forceinline__ void value(const Hermite &h, int k, float (&f)[CPL]) const
-    {
-#pragma unroll
-        for (int v = 0; v < CPL; ++v)
-            f[v] = fmaf(h.h00, v0[k][v], fmaf(h.h10, m0[k][v], fmaf(h.h01, v1[k][v], h.h11 * m1[k][v])));
-    }
-    // d/dt
-    __device__ __forceinline__ void slope(const Hermite &h, int k, float (&df)[CPL]) const
-    {
-#pragma unroll
-        for (int v = 0; v < CPL; ++v)
-            df[v] = fmaf(h.d00, v0[k][v], fmaf(h.d10, m0[k][v], fmaf(h.d01, v1[k][v], h.d11 * m1[k][v])));
-    }
-};
-
+// Radial tables come in two layouts: per knot the values and (knot-spacing-scaled) slopes of the 3
+// radial functions, [knot][value|slope][3][C] (`tables`, for row walkers that keep the two knots of
+// their current interval in registers), and per knot interval the monomial coefficients
+// (`tables_mono`, Horner form for kernels that visit intervals in no particular order).
 __device__ __forceinline__ int knot_of(float tx, int num_knots, float &t)
 {
     int kn = (int)tx;
     kn = kn > num_knots - 2 ? num_knots - 2 : kn;
     t = tx - (float)kn;
     return kn;
-}
-
-// Sum of four per-lane partials over the warp with 6 shuffles: returns, in lanes 0 / 16 / 8 / 24,
-// the warp totals of p0 / p1 / p2 / p3 (other lanes hold partial garbage).
-__device__ __forceinline__ float warp_sum4(float p0, float p1, float p2, float p3, int lane)
-{
-    float a = (lane & 16) ? p1 : p0, b = (lane & 16) ? p0 : p1;
-    a += __shfl_xor_sync(NNP_FULL_MASK, b, 16);
-    float c = (lane & 16) ? p3 : p2, e = (lane & 16) ? p2 : p3;
-    c += __shfl_xor_sync(NNP_FULL_MASK, e, 16);
-    float x = (lane & 8) ? c : a;
-    const float y = (lane & 8) ? a : c;
-    x += __shfl_xor_sync(NNP_FULL_MASK, y, 8);
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(NNP_FULL_MASK, x, o);
-    return x;
 }
 
 // Lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coordinate).
@@ -420,20 +349,6 @@ __global__ void k_normalize(const float *__restrict__ X, const float *__restrict
     st9(Xh + off, C, xh);
 }
 
-__global__ void k_node_product(const float *__restrict__ Mc, const float *__restrict__ Yc,
-                               float *__restrict__ Qc, int n, int C)
-{
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n * C) return;
-    const int node = idx / C, c = idx - node * C;
-    const size_t off = (size_t)node * 9 * C + c;
-    float m[9], y[9], q[9];
-    ld9(Mc + off, C, m);
-    ld9(Yc + off, C, y);
-    node_product_fwd(m, y, q);
-    st9(Qc + off, C, q);
-}
-
 // X_new = Xh + D + D*D, written either as X_new (last layer, read by the head) or directly as the
 // next layer's normalised input Xh' = X_new / (|X_new|^2 + 1) together with that norm.
 __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict__ Dc,
@@ -531,95 +446,9 @@ __global__ void k_embed_gate_bwd(const float *__restrict__ GX, const float *__re
 }
 
 // ----------------------------------------------------------------------- interaction edges
-// M_i = sum_e f_e[:,grp] * Yc_j   (f_e = table(u_e) * phi_e)
-template <int C, int CPL>
-__global__ void __launch_bounds__(256) k_edge_message(TnDev d, int layer)
-{
-    constexpr int NPARTS = C / (32 * CPL);
-    if (overflowed(d)) return;
-    const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int s = gw / NPARTS, part = gw - s * NPARTS;
-    if (s >= d.n) return;
-    const int cb = part * 32 * CPL + lane * CPL;
-    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
-    const float *Y = d.Yc[layer];
-    float acc[9][CPL];
-#pragma unroll
-    for (int q = 0; q < 9; ++q)
-#pragma unroll
-        for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
-    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
-    KnotCache<C, CPL> kc;
-    kc.init();
-    const int nk = d.m.num_knots;
-    // software pipeline: the sender row of edge e+1 is in flight while edge e is consumed
-    float y[9][CPL];
-    float4 ga = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 < e1) {
-        ga = d.geoA[e0];
-        const float *yj = Y + (size_t)d.col[e0] * 9 * C + cb;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) ldv<CPL>(yj + q * C, y[q]);
-    }
-    for (int e = e0; e < e1; ++e) {
-        float yn[9][CPL];
-        float4 gan = ga;
-        if (e + 1 < e1) {
-            gan = d.geoA[e + 1];
-            const float *yj = Y + (size_t)d.col[e + 1] * 9 * C + cb;
-#pragma unroll
-            for (int q = 0; q < 9; ++q) ldv<CPL>(yj + q * C, yn[q]);
-        }
-        float t;
-        const int kn = knot_of(ga.x, nk, t);
-        kc.seek(tab, kn, cb);
-        const float phi = ga.y;
-        const Hermite h = hermite_weights(t);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            float f[CPL];
-            kc.value(h, k, f);
-#pragma unroll
-            for (int v = 0; v < CPL; ++v) f[v] *= phi;
-            const int qa = k == 0 ? 0 : (k == 1 ? 1 : 4), qb = k == 0 ? 1 : (k == 1 ? 4 : 9);
-#pragma unroll
-            for (int q = qa; q < qb; ++q)
-#pragma unroll
-                for (int v = 0; v < CPL; ++v) acc[q][v] = fmaf(f[v], y[q][v], acc[q][v]);
-        }
-        ga = gan;
-#pragma unroll
-        for (int q = 0; q < 9; ++q)
-#pragma unroll
-            for (int v = 0; v < CPL; ++v) y[q][v] = yn[q][v];
-    }
-    float *out = d.Mc[layer] + (size_t)s * 9 * C + cb;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) stv<CPL>(out + q * C, acc[q]);
-    // node update fused in: Q = (M*Y + Y*M) / (|M*Y + Y*M|^2 + 1) for this node's channels
-    const float *yi = Y + (size_t)s * 9 * C + cb;
-    float yown[9][CPL], qv[9][CPL];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) ldv<CPL>(yi + q * C, yown[q]);
-#pragma unroll
-    for (int v = 0; v < CPL; ++v) {
-        float m9[9], y9[9], q9[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            m9[q] = acc[q][v];
-            y9[q] = yown[q][v];
-        }
-        node_product_fwd(m9, y9, q9);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) qv[q][v] = q9[q];
-    }
-    float *qo = d.Qc + (size_t)s * 9 * C + cb;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) stv<CPL>(qo + q * C, qv[q]);
-}
-
-// Knot cache restricted to the radial functions [K0, K0 + NG) (see KnotCache).
+// The two knots of a row walker's current table interval, for the radial functions [K0, K0 + NG):
+// rows are sorted by table coordinate, so moving on means "same interval" (no load), "next
+// interval" (one knot) or a jump (two knots) - a warp-uniform decision.
 template <int C, int CPL, int K0, int NG>
 struct KnotCacheG {
     float v0[NG][CPL], m0[NG][CPL], v1[NG][CPL], m1[NG][CPL];
@@ -1307,8 +1136,6 @@ GemmArgs plain_gemm(const float *A, const nnp_gemm_weight &W, const float *bias,
     GemmArgs g{};
     g.A = A;
     g.W = W.w;
-    g.Whi = W.hi;
-    g.Wlo = W.lo;
     g.bias = bias;
     g.out = out;
     g.aux = aux;
@@ -1331,8 +1158,6 @@ GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n,
         GemmArgs &g = b.g[k];
         g.A = A;
         g.W = W3[k].w;
-        g.Whi = W3[k].hi;
-        g.Wlo = W3[k].lo;
         g.out = out;
         g.out2 = out2;
         g.aux = aux;
@@ -1389,12 +1214,6 @@ int run_step(TnDev &d, cudaStream_t st)
     const int ew_blocks = nnp_blocks((int64_t)n * C, 256);
     const nnp_tn_model &m = d.m;
     const EdgeTuning &tune = edge_tuning();
-    static const int dbg_kn = env_int("NNP_DBG_KN", 0);
-    if (dbg_kn) d.m.num_knots = 2;
-    static const int dbg_col = env_int("NNP_DBG_COL", 0);
-    d.dbg_col = dbg_col;
-    static const int dbg_nosort = env_int("NNP_DBG_NOSORT", 0);
-    d.dbg_nosort = dbg_nosort;   // measurement only: every edge reads table interval 0
     {
         auto parts = [](int cpl) {
             if (cpl * 32 > C) cpl = C / 32;
@@ -1439,9 +1258,7 @@ int run_step(TnDev &d, cudaStream_t st)
         if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xm, d.e1, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
-        static const int fwd_split = env_int("NNP_FWD_SPLIT", 1);
-        if (fwd_split) { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); }
-        else { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); } 
+        { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); }
         GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + 3, d.Dc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
         { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, l + 1 < L ? d.Xh[l + 1] : nullptr, l + 1 < L ? d.nx[l + 1] : nullptr, n, C); }
@@ -1510,12 +1327,6 @@ int run_step(TnDev &d, cudaStream_t st)
     return NNP_OK;
 }
 
-__global__ void k_identity(const float *in, float *out, int n)
-{
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i];
-}
-
 }  // namespace
 
 extern "C" int nnp_tn_workspace_bytes(const nnp_tn_model *m, int32_t n_atoms, int32_t capacity,
@@ -1577,7 +1388,7 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = use_mma < 0 ? 0 : (use_mma > 5 ? 5 : use_mma);
+    g_nnp_gemm_use_mma = (use_mma == 5 || use_mma == 3 || use_mma == 1) ? use_mma : (use_mma <= 0 ? 0 : 5);
     return NNP_OK;
 }
 

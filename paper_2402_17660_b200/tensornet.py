@@ -180,46 +180,6 @@ def monomial_tables(tables: np.ndarray) -> np.ndarray:
     return mono.astype(np.float32)
 
 
-def gemm_tile_n(n_out: int) -> int:
-    """Output-tile width the tcgen05 kernel uses for a weight with ``n_out`` rows."""
-    for nt in (128, 64, 32, 16):
-        if n_out % nt == 0:
-            return nt
-    raise ValidationError(f"GEMM output width {n_out} must be a multiple of 16")
-
-
-def tf32_round(x: np.ndarray) -> np.ndarray:
-    """float32 -> nearest TF32 value (10-bit mantissa, ties away from zero, like cvt.rna.tf32)."""
-    bits = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    return ((bits + 0x1000) & 0xFFFFE000).astype(np.uint32).view(np.float32)
-
-
-def stage_gemm_weight(w: np.ndarray):
-    """Split W[N, K] into TF32 hi/lo parts and lay both out as the shared-memory tile images the
-    tcgen05 kernel bulk-copies: [N/NT][ceil(K/32)][NT rows][32 floats] with the eight 16-byte
-    chunks of every 128-byte row XOR-swizzled by (row % 8) (K-major SWIZZLE_128B)."""
-    w32 = np.ascontiguousarray(w, dtype=np.float32)
-    n, k = w32.shape
-    nt = gemm_tile_n(n)
-    nchunks = (k + 31) // 32
-    hi = tf32_round(w32)
-    lo = tf32_round(w32 - hi)
-    out = []
-    rows = np.arange(nt)
-    kk = np.arange(32)
-    # float index of (row r, k-in-chunk kk) inside one [NT][32] block
-    idx = ((rows[:, None] >> 3) * 256 + (rows[:, None] & 7) * 32
-           + (((kk[None, :] >> 2) ^ (rows[:, None] & 7)) << 2) + (kk[None, :] & 3))
-    for part in (hi, lo):
-        padded = np.zeros((n, nchunks * 32), dtype=np.float32)
-        padded[:, :k] = part
-        blocks = padded.reshape(n // nt, nt, nchunks, 32).transpose(0, 2, 1, 3)   # [tile][chunk][r][kk]
-        img = np.empty((n // nt, nchunks, nt * 32), dtype=np.float32)
-        img[:, :, idx.ravel()] = blocks.reshape(n // nt, nchunks, nt * 32)
-        out.append(img.ravel())
-    return w32, out[0], out[1]
-
-
 class _Plan:
     """Everything that is fixed for one input shape: buffers, neighbor engine, graph."""
 
@@ -277,8 +237,7 @@ class TensorNet:
         m.init_norm_g, m.init_norm_b = dev("ing", P["init_norm_g"]), dev("inb", P["init_norm_b"])
 
         def gemm_weight(slot, name, w):
-            w32, hi, lo = stage_gemm_weight(w)
-            slot.w, slot.hi, slot.lo = dev(name, w32), dev(name + ".hi", hi), dev(name + ".lo", lo)
+            slot.w = dev(name, w)
 
         gemm_weight(m.es0_w, "es0_w", P["es0_w"])
         gemm_weight(m.es0_wT, "es0_wT", P["es0_w"].T)
