@@ -365,12 +365,12 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
 
     if (tid == 0) {
         for (int s = 0; s < ST_STAGES; ++s) {
-            mbar_init(&full_bar[s], ST_PRODUCERS);
+            mbar_init(&full_bar[s], ST_PRODUCERS / 32);     // one arrival per producer warp
             mbar_init(&empty_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 32 * ST_EPI_WARPS);
+            mbar_init(&tempty_bar[a], ST_EPI_WARPS);        // one arrival per epilogue warp
         }
         mbar_init(&w_bar, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -460,7 +460,8 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
                 *reinterpret_cast<uint4 *>(x_lo + off[p]) = l;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&full_bar[s]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[s]);
         };
         for (int it = 0; it < total + ST_LAG; ++it) {
             if (it < total) issue(it);
@@ -580,7 +581,8 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
             }
             if (!waited) mbar_wait(&tfull_bar[acc], acc_ph);
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&tempty_bar[acc]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
