@@ -250,6 +250,7 @@ def main():
     ap.add_argument("--workload", default="C", choices=["A", "C", "D", "E"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-md", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -421,6 +422,27 @@ def main():
                        f"float64 numpy TensorNet oracle energy+forces on a 1000-atom periodic box of the "
                        f"same density ({t_tn:.1f} s, BLAS threads = all cores), scaled by 23558/1000"),
         }
+    if world == 1 and args.workload in ("A", "C") and not args.no_md:
+        # the MD driver = the same step + the Langevin integrator kernel in
+        # one graph, float64 positions resident on the device, noise from the device Philox
+        from paper_2402_17660_b200 import md as M
+
+        system = P.build_system(np.asarray(pos, dtype=np.float32).astype(np.float64), z, box=model._as_box(box))
+        state = M.initialize_state(system, 300.0, seed=0)
+        integ = M.DeviceIntegrator(model, system, state.velocities, state.masses, 300.0, seed=0)
+        integ.run_device(5, 0.5, 1.0)
+        torch.cuda.synchronize()
+        md_steps = max(10, args.steps // 2)
+        start.record()
+        integ.run_device(md_steps, 0.5, 1.0)
+        stop.record()
+        torch.cuda.synchronize()
+        integ.check_finite("in the MD bench")
+        md_ms = start.elapsed_time(stop) / md_steps
+        line["md"] = {"ms_per_step": round(md_ms, 4), "msteps_per_day": round(86.4 / md_ms, 3),
+                      "ns_per_day_at_1fs": round(86.4 / md_ms, 3), "steps": md_steps,
+                      "what": "neighbor search + TensorNet energy/forces + Langevin-middle integrator "
+                              "(device Philox noise), one CUDA graph per step, float64 state"}
     if world == 1 and not args.no_sweep:
         line["neighbor_sweep"] = neighbor_sweep(torch, peak_gbs)
     print(json.dumps(line))

@@ -178,6 +178,27 @@ int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_sampl
                          float *energy, float *forces, float *per_atom, void *workspace,
                          size_t workspace_bytes, nnp_stream_t stream);
 
+/* ------------------------------------------------------------------ MD integrator
+ * Replaces langevin_middle_step (md.py:114-145): kick, half drift, Ornstein-Uhlenbeck velocity
+ * mixing, half drift, in float64 with the reference's operation order (bit-identical to the NumPy
+ * statement for equal forces and noise).
+ *   pos, vel   [n,3] float64, updated in place       forces [n,3] float32 (the step's output)
+ *   acc_scale  [n]   float64 = FORCE_TO_ACCELERATION / m_i (units.py:26)
+ *   sigma      [n]   float64 = sqrt(k_B T FORCE_TO_ACCELERATION / m_i) (md.py:131-133)
+ *   noise      [n,3] float64 standard normals supplied by the caller (the reference's own
+ *              Philox stream), or NULL: drawn on the device from Philox4x32-10 keyed by
+ *              (seed, *step_counter, atom) with Box-Muller
+ *   step_counter device uint64 or NULL; incremented by the call, so a captured graph advances
+ *              the random stream by itself
+ *   c1 = exp(-gamma dt), c2 = sqrt(1 - c1^2) (md.py:128-129); c2 == 0 skips the mixing
+ *   pos32_out  optional [n,3] float32 copy of the new positions
+ *   nonfinite_flag optional device int32, set to 1 when a force is not finite (md.py:124-125)
+ */
+int nnp_md_langevin_middle(double *pos, double *vel, const float *forces, const double *acc_scale,
+                           const double *sigma, const double *noise, uint64_t seed,
+                           uint64_t *step_counter, double dt, double c1, double c2,
+                           float *pos32_out, int32_t *nonfinite_flag, int32_t n, nnp_stream_t stream);
+
 /* Test hook: out[M,N] = A[M,K] * W[N,K]^T (+ bias[N]) through the same tile engine the node
  * kernels use (3xTF32 tensor-core path or FP32 FFMA). */
 int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const float *bias, float *out,

@@ -13,5 +13,9 @@ from .neighbors import (
 )
 from .tensornet import TNConfig, TensorNet, build_radial_tables, init_params
 from .compose import ComposedPotential, evaluate, evaluate_auto
+from .md import (
+    MDState, Trajectory, default_masses, initialize_state, langevin_middle_step,
+    maxwell_boltzmann_velocities, rmsd, run_simulation, throughput,
+)
 
 __version__ = "0.1.0"

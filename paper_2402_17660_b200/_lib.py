@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "nnp_last_error", "nnp_version", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
     "nnp_distance_pullback", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
     "nnp_test_gemm_nt", "nnp_set_gemm_mode", "nnp_launch_count", "nnp_profile_begin",
-    "nnp_profile_report",
+    "nnp_profile_report", "nnp_md_langevin_middle",
 )
 
 _f = ctypes.c_float
@@ -105,6 +105,8 @@ def load() -> ctypes.CDLL:
     ]
     lib.nnp_test_gemm_nt.argtypes = [_p, ctypes.POINTER(GemmWeight), _p, _p, _i32, _i32, _i32, _p]
     lib.nnp_set_gemm_mode.argtypes = [ctypes.c_int]
+    dbl, u64 = ctypes.c_double, ctypes.c_uint64
+    lib.nnp_md_langevin_middle.argtypes = [_p, _p, _p, _p, _p, _p, u64, _p, dbl, dbl, dbl, _p, _p, _i32, _p]
     lib.nnp_launch_count.argtypes = [ctypes.c_int]
     lib.nnp_profile_begin.argtypes = []
     lib.nnp_profile_report.argtypes = [ctypes.c_char_p, ctypes.c_int]
@@ -112,7 +114,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         if name not in ("nnp_last_error",):
             fn.restype = ctypes.c_int
-    if "NNP_GEMM_MODE" in os.environ:       # 2 = tcgen05, 1 = mma.sync, 0 = FFMA (measurements)
+    if "NNP_GEMM_MODE" in os.environ:       # 5/3 = tcgen05, 1 = mma.sync, 0 = FFMA (measurements)
         lib.nnp_set_gemm_mode(int(os.environ["NNP_GEMM_MODE"]))
     _lib = lib
     return lib

@@ -357,7 +357,7 @@ class TensorNet:
         """
         torch = self._torch
         dev = self.device
-        pos_t = torch.as_tensor(pos)
+        pos_t = torch.as_tensor(np.array(pos) if isinstance(pos, np.ndarray) and not pos.flags.writeable else pos)
         if pos_t.dim() != 2 or pos_t.shape[1] != 3:
             raise ValidationError("positions must have shape (N, 3)")
         n = pos_t.shape[0]
@@ -365,7 +365,7 @@ class TensorNet:
             raise ValidationError("system must contain at least one atom")
         if pos_t.dtype not in (torch.float32, torch.float64):
             pos_t = pos_t.to(torch.float32)
-        z_t = torch.as_tensor(z)
+        z_t = torch.as_tensor(np.array(z) if isinstance(z, np.ndarray) and not z.flags.writeable else z)
         if z_t.shape != (n,):
             raise ValidationError(f"length mismatch: {n} positions but {tuple(z_t.shape)} species")
         if batch is None:
