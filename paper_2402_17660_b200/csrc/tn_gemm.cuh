@@ -185,22 +185,34 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0f;
 
+    // operand chunks are fetched one K step ahead (registers), so the global/L2 latency of chunk
+    // k+1 overlaps the tensor-core work on chunk k; small problems are pure latency otherwise
+    float4 av[2], wv[2];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            av[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            wv[i] = av[i];
+            const bool k_ok = k0 + a_k4[i] < g.K;
+            if (a_ptr[i] && k_ok) av[i] = *reinterpret_cast<const float4 *>(a_ptr[i] + k0);
+            if (w_ptr[i] && k_ok) wv[i] = __ldg(reinterpret_cast<const float4 *>(w_ptr[i] + k0));
+        }
+    };
+    fetch(0);
     for (int k0 = 0; k0 < g.K; k0 += GEMM_BK) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            float4 av = make_float4(0.f, 0.f, 0.f, 0.f), wv = av;
-            const bool k_ok = k0 + a_k4[i] < g.K;
-            if (a_ptr[i] && k_ok) av = *reinterpret_cast<const float4 *>(a_ptr[i] + k0);
-            if (w_ptr[i] && k_ok) wv = *reinterpret_cast<const float4 *>(w_ptr[i] + k0);
+            float4 a = av[i];
             if (PRO == PRO_SILU) {
-                av.x = nnp_silu(av.x);
-                av.y = nnp_silu(av.y);
-                av.z = nnp_silu(av.z);
-                av.w = nnp_silu(av.w);
+                a.x = nnp_silu(a.x);
+                a.y = nnp_silu(a.y);
+                a.z = nnp_silu(a.z);
+                a.w = nnp_silu(a.w);
             }
-            *reinterpret_cast<float4 *>(&As[a_row[i]][a_k4[i]]) = av;
-            *reinterpret_cast<float4 *>(&Ws[a_row[i]][a_k4[i]]) = wv;
+            *reinterpret_cast<float4 *>(&As[a_row[i]][a_k4[i]]) = a;
+            *reinterpret_cast<float4 *>(&Ws[a_row[i]][a_k4[i]]) = wv[i];
         }
+        if (k0 + GEMM_BK < g.K) fetch(k0 + GEMM_BK);
         __syncthreads();
         if (MMA) {
 #pragma unroll
