@@ -691,7 +691,11 @@ static int gemm_launch(const GemmBatch &b_in, int count, cudaStream_t stream)
     if (maxM <= 0) return NNP_OK;
     // a handful of row tiles (single small molecules) is pure launch latency: the mma.sync tile has
     // no TMEM allocation or weight staging to pay for (measured on the 22-atom config)
-    const bool tiny = g_nnp_gemm_use_mma == 5 && maxM <= 1024;
+    // ... and the per-tile tcgen05 kernel walks its K chunks serially (~2.5 us each), which is what
+    // a GEMM over N_atoms rows costs up to ~8k atoms; the mma.sync tile is quicker there
+    // (measured at 2 489 atoms: 0.15 vs 0.24 ms for the eight dense GEMMs)
+    const bool streamable = maxN == 128 && b.g[0].K == 128;
+    const bool tiny = g_nnp_gemm_use_mma == 5 && (maxM <= 1024 || (!streamable && maxM <= 8192));
     if (g_nnp_gemm_use_mma >= 2 && !tiny) {
         int rc = -100;
         if (g_nnp_gemm_use_mma == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);

@@ -1030,15 +1030,18 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
 }
 
 // forces: F_i = -sum_{e in row i} [ (g_d[e] + g_d[e']) u_e + (1 - u u^T)(g_u[e] - g_u[e']) / d_e ]
-// with e' the reverse edge (u_e' = -u_e), precomputed by k_edge_rev.
-__global__ void k_forces(TnDev d)
+// with e' the reverse edge (u_e' = -u_e), precomputed by k_edge_rev.  One warp per atom: lanes
+// take the row's edges 32 at a time (every edge costs a few dependent scattered reads), then a
+// fixed-order butterfly sums the three components, so the result is reproducible.
+__global__ void __launch_bounds__(256) k_forces(TnDev d)
 {
     if (overflowed(d)) return;
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= d.n) return;
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
-    for (int e = e0; e < e1; ++e) {
+    for (int e = e0 + lane; e < e1; e += 32) {
         const int j = d.col[e];
         if (j == s) continue;
         const int er = d.rev[e];
@@ -1058,10 +1061,15 @@ __global__ void k_forces(TnDev d)
         gy += gd * gb.y + (vy - gb.y * dot) * ga.w;
         gz += gd * gb.z + (vz - gb.z * dot) * ga.w;
     }
-    const size_t o = 3 * (size_t)(d.order ? d.order[s] : s);
-    d.forces[o] = -gx;
-    d.forces[o + 1] = -gy;
-    d.forces[o + 2] = -gz;
+    gx = nnp_warp_sum(gx);
+    gy = nnp_warp_sum(gy);
+    gz = nnp_warp_sum(gz);
+    if (lane == 0) {
+        const size_t o = 3 * (size_t)(d.order ? d.order[s] : s);
+        d.forces[o] = -gx;
+        d.forces[o + 1] = -gy;
+        d.forces[o + 2] = -gz;
+    }
 }
 
 __global__ void k_fill_int(int *p, int n, int v)
@@ -1321,7 +1329,7 @@ int run_step(TnDev &d, cudaStream_t st)
     }
     { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
     { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d, Gb))); }
-    { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(nnp_blocks(n, 128)), 128, 0, st>>>(d); }
+    { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
     return NNP_OK;
