@@ -15,7 +15,9 @@
 #include "tn_math.cuh"
 
 enum { PRO_NONE = 0, PRO_SILU = 1 };
-enum { EPI_STORE = 0, EPI_MUL_SILU_GRAD = 1, EPI_GATE = 2, EPI_ADD = 3 };
+enum { EPI_STORE = 0, EPI_MUL_SILU_GRAD = 1, EPI_GATE = 2, EPI_ADD = 3, EPI_STORE_SILU = 4 };
+// EPI_STORE_SILU: out = v (kept for the reverse sweep) and out2 = silu(v) (the next linear's input), so
+// that the activation is evaluated once per element instead of once per column tile of the consumer
 
 struct GemmArgs {
     const float *A;
@@ -90,6 +92,9 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs &g, int r, int c, f
     const size_t o = (size_t)pr * g.ldo + c;
     if (EPI == EPI_STORE) {
         g.out[o] = v;
+    } else if (EPI == EPI_STORE_SILU) {
+        g.out[o] = v;
+        g.out2[o] = nnp_silu(v);
     } else if (EPI == EPI_MUL_SILU_GRAD) {
         g.out[o] = v * nnp_silu_grad(g.aux[(size_t)pr * g.ldaux + c]);
     } else if (EPI == EPI_GATE) {
@@ -117,6 +122,9 @@ __device__ __forceinline__ void gemm_epilogue4(const GemmArgs &g, int r, int c, 
     const size_t o = (size_t)pr * g.ldo + c;
     if (EPI == EPI_STORE) {
         *reinterpret_cast<float4 *>(g.out + o) = v;
+    } else if (EPI == EPI_STORE_SILU) {
+        *reinterpret_cast<float4 *>(g.out + o) = v;
+        *reinterpret_cast<float4 *>(g.out2 + o) = make_float4(nnp_silu(v.x), nnp_silu(v.y), nnp_silu(v.z), nnp_silu(v.w));
     } else if (EPI == EPI_MUL_SILU_GRAD) {
         const float4 a = __ldg(reinterpret_cast<const float4 *>(g.aux + (size_t)pr * g.ldaux + c));
         v.x *= nnp_silu_grad(a.x);

@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
             int comp = ncomp > 0 ? r0 - node * ncomp : 0;
             const size_t prow = ncomp > 0 ? (size_t)node * 9 + g.q0 + comp : (size_t)r0;
             float *po = g.out + prow * ldo + n;             // element (row r0, channel n); ldaux == ldo
-            float *po2 = EPI == EPI_GATE ? g.out2 + prow * ldo + n : nullptr;
+            float *po2 = (EPI == EPI_GATE || EPI == EPI_STORE_SILU) ? g.out2 + prow * ldo + n : nullptr;
             const float *pa = (EPI == EPI_ADD || EPI == EPI_MUL_SILU_GRAD) ? g.aux + prow * ldo + n : nullptr;
             const float *pg = EPI == EPI_GATE ? g.aux + (size_t)node * g.ldaux + 3 * n + g.grp : nullptr;
             int off = 0, goff = 0;                          // running element offsets from po / pg
@@ -568,6 +568,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
                         const float x = v[i] + bias;
                         if (EPI == EPI_STORE) {
                             po[o[i]] = x;
+                        } else if (EPI == EPI_STORE_SILU) {
+                            po[o[i]] = x;
+                            po2[o[i]] = nnp_silu(x);
                         } else if (EPI == EPI_ADD) {
                             po[o[i]] = x + a[i];
                         } else if (EPI == EPI_MUL_SILU_GRAD) {

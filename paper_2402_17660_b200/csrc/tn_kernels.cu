@@ -79,10 +79,10 @@ struct TnDev {
     float4 *g_u;   // [NNP_PARTS][capacity] dE/du_e
     // workspace: nodes
     int *zs, *sample_ptr;
-    float *X0, *n0, *ln0, *e0, *e1, *Xm, *Xa, *Xb;
+    float *X0, *n0, *ln0, *e0, *se0, *e1, *Xm, *Xa, *Xb;   // se0 = silu(e0), sr0 = silu(r0)
     float *Xh[NNP_TN_MAX_LAYERS], *nx[NNP_TN_MAX_LAYERS], *Yc[NNP_TN_MAX_LAYERS],
         *Mc[NNP_TN_MAX_LAYERS], *Dc[NNP_TN_MAX_LAYERS];
-    float *Qc, *lnr, *r0, *r1, *e_atom;
+    float *Qc, *lnr, *r0, *sr0, *r1, *e_atom;
     float *G1, *G2, *G3;  // [N,9,C] gradient scratch
     float *g_r1, *g_r0, *g_lnr, *g_e1, *g_e0, *g_ln0;
 };
@@ -1098,6 +1098,7 @@ size_t carve(TnDev &d, void *ws)
     d.n0 = ar.take<float>(n * C);
     d.ln0 = ar.take<float>(n * C);
     d.e0 = ar.take<float>(n * 2 * C);
+    d.se0 = ar.take<float>(n * 2 * C);
     d.e1 = ar.take<float>(n * 3 * C);
     d.Xm = ar.take<float>(T);
     d.Xa = ar.take<float>(T);
@@ -1112,6 +1113,7 @@ size_t carve(TnDev &d, void *ws)
     d.Qc = ar.take<float>(T);
     d.lnr = ar.take<float>(n * 3 * C);
     d.r0 = ar.take<float>(n * C);
+    d.sr0 = ar.take<float>(n * C);
     d.r1 = ar.take<float>(n * (C / 2));
     d.e_atom = ar.take<float>(n);
     d.G1 = ar.take<float>(T);
@@ -1248,9 +1250,10 @@ int run_step(TnDev &d, cudaStream_t st)
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.ln0, m.es0_w, m.es0_b, d.e0, n, 2 * C, C);
+        b.g[0].out2 = d.se0;
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE_SILU>(b, 1, st))); }
+        b.g[0] = plain_gemm(d.se0, m.es1_w, m.es1_b, d.e1, n, 3 * C, 2 * C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
-        b.g[0] = plain_gemm(d.e0, m.es1_w, m.es1_b, d.e1, n, 3 * C, 2 * C);
-        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
         if (L == 0) {
             GemmBatch mx = mix_gemm(d.X0, m.et_w, d.Xa, n, C, d.Xm, d.e1, 3 * C);
             { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_GATE>(mx, 3, st))); }
@@ -1278,9 +1281,10 @@ int run_step(TnDev &d, cudaStream_t st)
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.lnr, m.lin_w, m.lin_b, d.r0, n, C, 3 * C);
+        b.g[0].out2 = d.sr0;
+        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE_SILU>(b, 1, st))); }
+        b.g[0] = plain_gemm(d.sr0, m.h1_w, m.h1_b, d.r1, n, H, C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
-        b.g[0] = plain_gemm(d.r0, m.h1_w, m.h1_b, d.r1, n, H, C);
-        { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_SILU, EPI_STORE>(b, 1, st))); }
     }
     { NNP_PROF("k_head", st); k_head<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, H); }
     { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), (n / d.n_samples >= 2048 ? 1024 : 256), 0, st>>>(d); }
