@@ -977,6 +977,8 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         nga = d.geoA[e0];
         ngb = d.geoB[e0];
     }
+    float kd = 0.0f;
+    float4 ku = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int e = e0; e < e1; ++e) {
         const int j = nj, zj = nz;
         const float4 ga = nga, gb = ngb;
@@ -986,7 +988,8 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
             nga = d.geoA[e + 1];
             ngb = d.geoB[e + 1];
         }
-        if (j == s) continue;  // a self loop has no geometry
+        // (a self loop has no geometry: its zero envelope derivative and unit vector make every
+        //  term below vanish, and the flush skips its slot)
         float zsnd[CPL];
         ldv<CPL>(d.m.z_send + (size_t)zj * C + cb, zsnd);
         float f[3][CPL], df[3][CPL];
@@ -1022,9 +1025,18 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         px = nnp_warp_sum(px);
         py = nnp_warp_sum(py);
         pz = nnp_warp_sum(pz);
-        if (lane == 0) {
-            d.g_d[(size_t)part * d.capacity + e] += pd;
-            d.g_u[(size_t)part * d.capacity + e] = make_float4(2.0f * px, 2.0f * py, 2.0f * pz, 0.0f);
+        // every lane holds the four totals; lane (e - e0) % 32 keeps them, and a full group of 32
+        // edges is written with one coalesced store instead of 32 single-lane ones
+        if (lane == ((e - e0) & 31)) {
+            kd = pd;
+            ku = make_float4(2.0f * px, 2.0f * py, 2.0f * pz, 0.0f);
+        }
+        if (((e - e0) & 31) == 31 || e + 1 == e1) {
+            const int eb = e0 + ((e - e0) & ~31) + lane;      // this lane's edge of the group
+            if (eb <= e && d.col[eb] != s) {
+                d.g_d[(size_t)part * d.capacity + eb] += kd;
+                d.g_u[(size_t)part * d.capacity + eb] = ku;
+            }
         }
     }
 }
