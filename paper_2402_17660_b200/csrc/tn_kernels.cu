@@ -1021,10 +1021,21 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
             py = fmaf(w1, G[2][v], fmaf(w2, vy, py));
             pz = fmaf(w1, G[3][v], fmaf(w2, vz, pz));
         }
-        pd = nnp_warp_sum(pd);
-        px = nnp_warp_sum(px);
-        py = nnp_warp_sum(py);
-        pz = nnp_warp_sum(pz);
+        {   // four warp sums with 6 + 4 shuffles instead of 20: transpose-reduce, then broadcast
+            float a = (lane & 16) ? px : pd, b = (lane & 16) ? pd : px;
+            a += __shfl_xor_sync(NNP_FULL_MASK, b, 16);
+            float c = (lane & 16) ? pz : py, f2 = (lane & 16) ? py : pz;
+            c += __shfl_xor_sync(NNP_FULL_MASK, f2, 16);
+            float x = (lane & 8) ? c : a;
+            const float y = (lane & 8) ? a : c;
+            x += __shfl_xor_sync(NNP_FULL_MASK, y, 8);
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) x += __shfl_xor_sync(NNP_FULL_MASK, x, o);
+            pd = __shfl_sync(NNP_FULL_MASK, x, 0);
+            px = __shfl_sync(NNP_FULL_MASK, x, 16);
+            py = __shfl_sync(NNP_FULL_MASK, x, 8);
+            pz = __shfl_sync(NNP_FULL_MASK, x, 24);
+        }
         // every lane holds the four totals; lane (e - e0) % 32 keeps them, and a full group of 32
         // edges is written with one coalesced store instead of 32 single-lane ones
         if (lane == ((e - e0) & 31)) {
