@@ -75,7 +75,8 @@ struct TnDev {
     int *col, *rev, *newpos;
     float4 *geoA;  // (table coordinate, phi, dphi/dd, 1/d)
     float4 *geoB;  // (ux, uy, uz, u = exp(cutoff_lower - d))
-    float *g_d;    // [NNP_PARTS][capacity] dE/dd_e, one slot per channel part (summed in k_forces)
+    float *g_d;    // [(L+1) * nparts][capacity] dE/dd_e: one slot per (writing kernel, channel part), so every
+                   // kernel stores its share without a read-modify-write; summed in k_forces
     float4 *g_u;   // [NNP_PARTS][capacity] dE/du_e
     // workspace: nodes
     int *zs, *sample_ptr;
@@ -149,10 +150,8 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
         d.geoA[p] = make_float4(tx, phi, dphi, invd);
         d.geoB[p] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
                                 d.deltas[3 * (size_t)e + 2] * invd, u);
-        for (int q = 0; q < d.nparts; ++q) {
-            d.g_d[(size_t)q * d.capacity + p] = 0.0f;
-            d.g_u[(size_t)q * d.capacity + p] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int q = 0; q < d.nparts; ++q) d.g_u[(size_t)q * d.capacity + p] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < d.nparts * (d.m.num_layers + 1); ++q) d.g_d[(size_t)q * d.capacity + p] = 0.0f;
     }
 }
 
@@ -607,7 +606,7 @@ __global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
 // Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
 // is a gather over a's own row):
 //   G_Y[a] += sum_e f_e[:,grp] * G_M[b]                         (b = sender of e)
-//   slot e of g_d += sum_c sum_k <G_M[b], Yc[a]>_k * d f_e[c,k]/dd
+//   slot e of this launch's g_d = sum_c sum_k <G_M[b], Yc[a]>_k * d f_e[c,k]/dd
 // The second line is dE/dd of the REVERSE edge (a sends to b): the force kernel only ever uses
 // g_d[e] + g_d[reverse(e)], which is symmetric, so storing the reverse edge's term in slot e is
 // equivalent and needs no second gather (G_M[b] is already in registers, Yc[a] is the own node).
@@ -615,7 +614,7 @@ __global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
 // (launched with 128 threads: at 168 registers three blocks = 12 warps stay resident per SM)
 template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
-                                                          float *GY)
+                                                          float *GY, float *gd_layer)
 {
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
@@ -636,7 +635,7 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
         }
     }
     const float inv_step = 1.0f / d.m.u_step;
-    float *gd_slot = d.g_d + (size_t)part * d.capacity;
+    float *gd_slot = gd_layer + (size_t)part * d.capacity;   // this launch's own slots
     const int nk = d.m.num_knots;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
     for (int e = e0; e < e1; e += 2) {
@@ -730,8 +729,8 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
         x += __shfl_xor_sync(NNP_FULL_MASK, y, 16);
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(NNP_FULL_MASK, x, o);
-        if (lane == 0 && j0 != s) gd_slot[e] += x;
-        if (lane == 16 && two && j1 != s) gd_slot[e + 1] += x;
+        if (lane == 0 && j0 != s) gd_slot[e] = x;
+        if (lane == 16 && two && j1 != s) gd_slot[e + 1] = x;
     }
     float *out = GY + (size_t)s * 9 * C + cb;
 #pragma unroll
@@ -1045,7 +1044,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
         if (((e - e0) & 31) == 31 || e + 1 == e1) {
             const int eb = e0 + ((e - e0) & ~31) + lane;      // this lane's edge of the group
             if (eb <= e && d.col[eb] != s) {
-                d.g_d[(size_t)part * d.capacity + eb] += kd;
+                d.g_d[(size_t)part * d.capacity + eb] = kd;      // slot 0 .. nparts-1: the embedding's
                 d.g_u[(size_t)part * d.capacity + eb] = ku;
             }
         }
@@ -1074,10 +1073,13 @@ __global__ void __launch_bounds__(256) k_forces(TnDev d)
         for (int p = 0; p < d.nparts; ++p) {
             const size_t po = (size_t)p * d.capacity;
             const float4 ue = d.g_u[po + e], ur = d.g_u[po + er];
-            gd += d.g_d[po + e] + d.g_d[po + er];
             vx += ue.x - ur.x;
             vy += ue.y - ur.y;
             vz += ue.z - ur.z;
+        }
+        for (int p = 0; p < d.nparts * (d.m.num_layers + 1); ++p) {
+            const size_t po = (size_t)p * d.capacity;
+            gd += d.g_d[po + e] + d.g_d[po + er];
         }
         const float dot = vx * gb.x + vy * gb.y + vz * gb.z;
         gx += gd * gb.x + (vx - gb.x * dot) * ga.w;
@@ -1113,7 +1115,7 @@ size_t carve(TnDev &d, void *ws)
     d.newpos = ar.take<int>(cap);
     d.geoA = ar.take<float4>(cap);
     d.geoB = ar.take<float4>(cap);
-    d.g_d = ar.take<float>(cap * NNP_PARTS);
+    d.g_d = ar.take<float>(cap * NNP_PARTS * (size_t)(L + 1));
     d.g_u = ar.take<float4>(cap * NNP_PARTS);
     d.zs = ar.take<int>(n);
     d.sample_ptr = ar.take<int>((size_t)d.n_samples + 1);
@@ -1335,7 +1337,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc))); } 
+        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.nparts * d.capacity))); } 
         // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }
