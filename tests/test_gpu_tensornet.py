@@ -269,3 +269,46 @@ def test_config_c_full_size_properties():
                                            pr, dl, ds, want_forces=False)
     err = np.max(np.abs(per_atom[sub[inner]] - pa_ref[inner]))
     assert err < 5e-6, f"per-atom energy error {err:.3e}"
+
+
+def test_config_d_full_size_properties():
+    """8 192 molecules (~147 k atoms): finite, every molecule's forces sum to zero, per-atom energies
+    sum to the sample energies, and the first molecules evaluated on their own give the same numbers
+    (batch independence at full size; brute strategy inside each sample)."""
+    z, pos, batch, _ = synth.config_d_molecules(8192)
+    ns = int(batch[-1]) + 1
+    model = P.TensorNet(embedding_dimension=128, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=0)
+    zt, pt, bt = torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch)
+    e, f = model(zt, pt, bt)
+    assert e.shape == (ns,) and torch.isfinite(e).all() and torch.isfinite(f).all()
+    net = torch.zeros((ns, 3), device=f.device).index_add_(0, bt.to(f.device), f)
+    assert float(net.abs().max()) < 2e-5 * max(float(f.abs().max()), 1.0)
+    per_atom = model.last_per_atom_energy(len(pos), ns)
+    sums = torch.zeros(ns, device=f.device).index_add_(0, bt.to(f.device), per_atom)
+    assert torch.allclose(sums, e, rtol=2e-6, atol=1e-5)
+    sel = batch < 16
+    e_sub, f_sub = model(zt[sel], pt[sel], bt[sel])
+    assert torch.allclose(e[:16], e_sub, rtol=1e-6, atol=1e-6)
+    assert torch.allclose(f[: int(sel.sum())], f_sub, rtol=1e-5, atol=1e-7)
+    # and against the float64 oracle on those 16 molecules
+    e_ref, f_ref, _ = oracle_eval(model, z[sel], pos[sel], batch[sel], None)
+    assert np.max(np.abs(e_sub.cpu().numpy() - e_ref) / np.maximum(np.abs(e_ref), 1.0)) < E_TOL
+    assert np.max(np.abs(f_sub.cpu().numpy() - f_ref)) / np.max(np.abs(f_ref)) < F_TOL
+
+
+def test_config_e_full_size_properties():
+    """100 000 atoms in the triclinic box, 3 layers: finite, deterministic, zero net force, and
+    invariant under a rigid shift of all atoms (which re-wraps them through the periodic images and
+    reorders the cell lists): energy to 1e-6, forces to 1e-4 relative."""
+    z, pos, batch, box = synth.config_e_triclinic()
+    model = P.TensorNet(embedding_dimension=128, num_layers=3, num_rbf=32, cutoff_upper=5.0, seed=0)
+    zt = torch.as_tensor(z)
+    e1, f1 = model(zt, torch.as_tensor(pos, dtype=torch.float32), None, box)
+    e2, f2 = model(zt, torch.as_tensor(pos, dtype=torch.float32), None, box)
+    assert torch.isfinite(e1).all() and torch.isfinite(f1).all()
+    assert torch.equal(e1, e2) and torch.equal(f1, f2)
+    assert float(f1.sum(0).abs().max()) < 1e-3 * float(f1.abs().max()) * 100
+    shifted = (pos + np.array([3.7, -11.3, 27.9])).astype(np.float32)
+    e3, f3 = model(zt, torch.as_tensor(shifted), None, box)
+    assert abs(float(e3[0] - e1[0])) / abs(float(e1[0])) < 2e-6
+    assert float((f3 - f1).abs().max() / f1.abs().max()) < 2e-4   # float32 positions move by ~1e-6 A
