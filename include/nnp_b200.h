@@ -199,6 +199,33 @@ int nnp_md_langevin_middle(double *pos, double *vel, const float *forces, const 
                            uint64_t *step_counter, double dt, double c1, double c2,
                            float *pos32_out, int32_t *nonfinite_flag, int32_t n, nnp_stream_t stream);
 
+/* ------------------------------------------------------------------ analytic pair priors
+ * Replaces the pair functions and the assembly of priors.py:61-88,139-148,170-185,222-245 on a
+ * device neighbor list (float64 deltas / distances as nnp_nl_build writes them).  Every undirected
+ * pair gives half of its energy to each endpoint and equal and opposite forces; a directed list is
+ * reduced to rows with i < j, self loops are skipped.  Per-atom inputs are prepared by the host:
+ *   charge [n] partial charges (Coulomb); znum [n] atomic numbers as float64 and zpow [n] = Z^0.23
+ *   (ZBL); c6 [n] (eV A^6) and rvdw [n] (A) (D2).  per_atom [n] and forces [n,3] (may be NULL) are
+ *   float64 and are zeroed by the call.  count_dev (device int32, e.g. the list's counts[0]) overrides
+ *   count_host as the number of valid rows when not NULL; count_host then only sizes the launch. */
+#define NNP_PRIOR_COULOMB 1
+#define NNP_PRIOR_ZBL 2
+#define NNP_PRIOR_D2 4
+typedef struct nnp_prior_params {
+    int32_t flags;            /* NNP_PRIOR_* */
+    int32_t reserved;
+    double cutoff_upper;      /* the list's cutoff: cosine envelope of ZBL and D2 (priors.py:176,229) */
+    double coulomb_constant;  /* eV A / e^2 (units.py:13) */
+    double switch_radius;     /* Coulomb short-range switch (priors.py:124) */
+    double zbl_prefactor;     /* 0.8854 a0 (priors.py:44) */
+    double d2_s6, d2_steep;   /* priors.py:200-201 */
+} nnp_prior_params;
+int nnp_priors_pair_terms(const nnp_prior_params *p, const int32_t *pairs, const double *deltas,
+                          const double *dists, const int32_t *count_dev, int32_t count_host,
+                          int32_t full_list, const double *charge, const double *znum, const double *zpow,
+                          const double *c6, const double *rvdw, int32_t n_atoms, double *per_atom,
+                          double *forces, nnp_stream_t stream);
+
 /* Test hook: out[M,N] = A[M,K] * W[N,K]^T (+ bias[N]) through the same tile engine the node
  * kernels use (3xTF32 tensor-core path or FP32 FFMA). */
 int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const float *bias, float *out,

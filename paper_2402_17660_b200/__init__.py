@@ -12,6 +12,7 @@ from .neighbors import (
     build_with_auto_capacity, canonicalize, capacity_heuristic, distance_pullback,
 )
 from .tensornet import TNConfig, TensorNet, build_radial_tables, init_params
+from .priors import Atomref, Coulomb, D2Dispersion, PriorStack, PriorTerm, ZBL, evaluate_prior_stack
 from .compose import ComposedPotential, evaluate, evaluate_auto
 from .md import (
     MDState, Trajectory, default_masses, initialize_state, langevin_middle_step,

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "nnp_last_error", "nnp_version", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
     "nnp_distance_pullback", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
     "nnp_test_gemm_nt", "nnp_set_gemm_mode", "nnp_launch_count", "nnp_profile_begin",
-    "nnp_profile_report", "nnp_md_langevin_middle",
+    "nnp_profile_report", "nnp_md_langevin_middle", "nnp_priors_pair_terms",
 )
 
 _f = ctypes.c_float
@@ -42,6 +42,15 @@ class NlParams(ctypes.Structure):
         ("cutoff_lower", ctypes.c_double), ("cutoff_upper", ctypes.c_double),
         ("box", ctypes.c_double * 9), ("inv_box", ctypes.c_double * 9),
     ]
+
+
+class PriorParams(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_int32), ("reserved", ctypes.c_int32), ("cutoff_upper", ctypes.c_double),
+                ("coulomb_constant", ctypes.c_double), ("switch_radius", ctypes.c_double),
+                ("zbl_prefactor", ctypes.c_double), ("d2_s6", ctypes.c_double), ("d2_steep", ctypes.c_double)]
+
+
+PRIOR_COULOMB, PRIOR_ZBL, PRIOR_D2 = 1, 2, 4
 
 
 class GemmWeight(ctypes.Structure):
@@ -106,6 +115,8 @@ def load() -> ctypes.CDLL:
     lib.nnp_test_gemm_nt.argtypes = [_p, ctypes.POINTER(GemmWeight), _p, _p, _i32, _i32, _i32, _p]
     lib.nnp_set_gemm_mode.argtypes = [ctypes.c_int]
     dbl, u64 = ctypes.c_double, ctypes.c_uint64
+    lib.nnp_priors_pair_terms.argtypes = [ctypes.POINTER(PriorParams), _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _p,
+                                          _i32, _p, _p, _p]
     lib.nnp_md_langevin_middle.argtypes = [_p, _p, _p, _p, _p, _p, u64, _p, dbl, dbl, dbl, _p, _p, _i32, _p]
     lib.nnp_launch_count.argtypes = [ctypes.c_int]
     lib.nnp_profile_begin.argtypes = []

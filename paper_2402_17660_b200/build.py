@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libnnp_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
-SOURCES = ("scan.cu", "nl_kernels.cu", "tn_kernels.cu", "md_kernels.cu")
+SOURCES = ("scan.cu", "nl_kernels.cu", "tn_kernels.cu", "md_kernels.cu", "prior_kernels.cu")
 HEADERS = ("nnp_common.cuh", "tn_math.cuh", "tn_gemm.cuh", "tn_gemm_tc5.cuh", os.path.join("..", "..", "include", "nnp_b200.h"))
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
     float kd = 0.0f;
     float4 ku = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int e = e0; e < e1; ++e) {
-        const int j = nj, zj = nz;
+        const int zj = nz;
         const float4 ga = nga, gb = ngb;
         if (e + 1 < e1) {
             nj = d.col[e + 1];
