@@ -1,7 +1,7 @@
 """Accuracy and speed of the radial tables vs number of knots (config C, GPU box)."""
 import json, os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_17660_b200 as P
 from paper_2402_17660_b200 import synth
 z, pos, batch, box = synth.config_c_box()

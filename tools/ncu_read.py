@@ -1,4 +1,4 @@
-"""Summarise an .ncu-rep: python tools_ncu_read.py gpurun_out/x.ncu-rep [metric-substring ...]"""
+"""Summarise an .ncu-rep: python tools/ncu_read.py gpurun_out/x.ncu-rep [metric-substring ...]"""
 import csv, subprocess, sys, io
 rep = sys.argv[1]
 extra = sys.argv[2:]

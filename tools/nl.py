@@ -1,7 +1,7 @@
 """Neighbor-build kernel breakdown (GPU box)."""
 import json, sys, os
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_17660_b200 as P
 from paper_2402_17660_b200 import _lib, synth
 from paper_2402_17660_b200.neighbors import NeighborEngine, plan_strategy

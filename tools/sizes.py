@@ -1,7 +1,7 @@
 """Step time vs atom count for periodic boxes at the density of config C (GPU box)."""
 import json, os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_17660_b200 as P
 from paper_2402_17660_b200 import synth
 model = P.TensorNet(embedding_dimension=128, num_layers=2, num_rbf=32, cutoff_upper=5.0, seed=0)

@@ -1,7 +1,7 @@
 """Per-kernel timing of one config-C step under the current NNP_* environment (GPU box)."""
 import json, os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_17660_b200 as P
 from paper_2402_17660_b200 import _lib, synth
 

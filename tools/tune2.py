@@ -1,7 +1,7 @@
 """Per-kernel timing at a given atom count (periodic box at config-C density)."""
 import json, os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_17660_b200 as P
 from paper_2402_17660_b200 import _lib, synth
 n = int(sys.argv[1])
