@@ -288,5 +288,5 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
     }
 }
 
-extern int g_nnp_gemm_use_mma;  // 3 = tcgen05 3xTF32, one tile per CTA, 3 CTAs/SM (default);
-                                // 2 = persistent warp-specialised tcgen05; 1 = mma.sync 3xTF32; 0 = FP32 FFMA
+extern int g_nnp_gemm_use_mma;  // 5 = streaming tcgen05 for the 128 x 128 mixes, per-tile tcgen05 otherwise (default);
+                                // 3 = per-tile tcgen05 3xTF32; 1 = mma.sync 3xTF32; 0 = FP32 FFMA

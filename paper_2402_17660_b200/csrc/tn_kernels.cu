@@ -9,7 +9,8 @@
 //
 // Data layout: node tensors are [N][9][C] float32 (irreducible components, channel fastest);
 // a warp owns one node and each lane C/32 consecutive channels, so every row/gather access is a
-// full-width coalesced vector load.  Edges are CSR by receiver, sorted by (receiver, sender).
+// full-width coalesced vector load.  Edges arrive CSR by receiver, sorted by (receiver, sender);
+// the step re-sorts every row by distance (k_edge_order) and stores each edge's reverse edge.
 // Radial functions (distance projections of the embedding, radial MLP of each layer) are read
 // from per-layer cubic-Hermite tables in u = exp(cutoff_lower - d), built by the host in
 // float64: they depend on the distance only, so tabulating them removes the per-edge MLP
