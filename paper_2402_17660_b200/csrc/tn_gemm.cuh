@@ -29,7 +29,6 @@ struct GemmArgs {
     int M, N, K;
     int lda, ldo, ldaux;
     int ncomp, q0, grp;  // ncomp > 0: logical row r -> physical row (r / ncomp) * 9 + q0 + r % ncomp
-    int dbg;             // measurement switches (NNP_GEMM_DBG): 1 skip loads, 2 skip MMAs, 4 skip stores
 };
 
 struct GemmBatch {

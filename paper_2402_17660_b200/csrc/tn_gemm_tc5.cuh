@@ -675,13 +675,8 @@ static int launch(const GemmBatch &b, int count, cudaStream_t stream)
 }  // namespace tc5
 
 template <int PRO, int EPI>
-static int gemm_launch(const GemmBatch &b_in, int count, cudaStream_t stream)
+static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
 {
-    GemmBatch b = b_in;
-    {
-        static const int dbg = getenv("NNP_GEMM_DBG") ? atoi(getenv("NNP_GEMM_DBG")) : 0;
-        for (int i = 0; i < count; ++i) b.g[i].dbg = dbg;
-    }
     int maxM = 0, maxN = 0;
     for (int i = 0; i < count; ++i) {
         maxM = b.g[i].M > maxM ? b.g[i].M : maxM;
