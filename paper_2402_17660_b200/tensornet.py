@@ -184,7 +184,7 @@ class _Plan:
     """Everything that is fixed for one input shape: buffers, neighbor engine, graph."""
 
     __slots__ = ("key", "n", "n_samples", "capacity", "engine", "workspace", "z", "batch", "pos32",
-                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box")
+                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box", "batch_is_zero")
 
 
 class TensorNet:
@@ -298,6 +298,7 @@ class TensorNet:
         plan.workspace = torch.empty(need.value, dtype=torch.uint8, device=dev)
         plan.z = torch.zeros(n, dtype=torch.int32, device=dev)
         plan.batch = torch.zeros(n, dtype=torch.int32, device=dev)
+        plan.batch_is_zero = True
         plan.pos32 = torch.zeros((n, 3), dtype=torch.float32, device=dev) if pos_is_f32 else None
         plan.pos64 = torch.zeros((n, 3), dtype=torch.float64, device=dev)
         plan.energy = torch.zeros(n_samples, dtype=torch.float32, device=dev)
@@ -380,16 +381,22 @@ class TensorNet:
         capacity = self._capacity_hint.get((n, n_samples), self.neighbor_capacity(n))
         for _ in range(32):
             plan = self._plan(n, n_samples, box_obj, capacity, pos_t.dtype == torch.float32)
+            if check:
+                # species range check on whichever side the codes already live (host tensors: no
+                # device reduction and no extra synchronisation per call)
+                z_max = int(z_t.max())
+                if z_max >= self.config.max_z:
+                    raise ValidationError(
+                        f"species code {z_max} is out of range for max_z={self.config.max_z}")
             plan.z.copy_(z_t.to(device=dev, dtype=torch.int32, non_blocking=True))
-            if batch_t is None:
-                plan.batch.zero_()
-            else:
+            if batch_t is not None:
                 plan.batch.copy_(batch_t.to(device=dev, dtype=torch.int32, non_blocking=True))
+                plan.batch_is_zero = False
+            elif not plan.batch_is_zero:
+                plan.batch.zero_()
+                plan.batch_is_zero = True
             (plan.pos32 if plan.pos32 is not None else plan.pos64).copy_(
                 pos_t.to(device=dev, non_blocking=True))
-            if check and int(plan.z.max()) >= self.config.max_z:
-                raise ValidationError(
-                    f"species code {int(plan.z.max())} is out of range for max_z={self.config.max_z}")
             self._launch(plan)
             if not check:
                 break
