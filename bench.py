@@ -391,6 +391,23 @@ def main():
     if os.path.exists(traffic_path) and args.workload == "C":   # the ncu captures are of config C
         with open(traffic_path) as fh:
             roof["traffic"] = json.load(fh).get(dominant)
+    # the channel-mixing GEMMs against the tensor roofline (3xTF32: three tcgen05.mma kind::tf32 per
+    # product; TF32 peak taken as half of the measured dense bf16 peak, the nominal ratio)
+    gemm_roof = None
+    if "gemm_mix" in prof and prof["gemm_mix"][1] > 0:
+        per_launch_ms = prof["gemm_mix"][0] / prof["gemm_mix"][1]
+        flops = 2.0 * 9 * n_atoms * CHANNELS * CHANNELS * 3
+        tf32_peak = None
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(peaks_path):
+            with open(peaks_path) as fh:
+                tf32_peak = 0.5 * float(json.load(fh).get("bf16_tflops_sustained", 0.0)) or None
+        tf32_peak = tf32_peak or 0.5 * 1400.0
+        achieved = flops / (per_launch_ms * 1e-3) / 1e12
+        gemm_roof = {"bound": "tensor", "kernel": "gemm_mix (tcgen05 kind::tf32, 3xTF32)", "achieved": round(achieved, 1),
+                     "peak": round(tf32_peak, 1), "unit": "TFLOP/s", "frac": round(achieved / tf32_peak, 4),
+                     "hbm_frac": round(per_kernel_bytes["gemm_mix"] / (per_launch_ms * 1e-3) / 1e9 / peak_gbs, 4),
+                     "launches_per_step": prof["gemm_mix"][1], "avg_launch_ms": round(per_launch_ms, 5)}
     step_roof = {"algorithmic_bytes": step_bytes + nl_bytes,
                  "achieved_gbs": round((step_bytes + nl_bytes) / (ms_per_step * 1e-3) / 1e9, 1),
                  "frac": round((step_bytes + nl_bytes) / (ms_per_step * 1e-3) / 1e9 / peak_gbs, 4)}
@@ -412,6 +429,7 @@ def main():
         "launches_per_step": launches_per_step,
         "roofline": roof,
         "step_roofline": step_roof,
+        "gemm_roofline": gemm_roof,
         "kernel_ms": kernel_ms,
     }
     if world == 1 and not args.no_cpu and args.workload == "C":
