@@ -101,9 +101,14 @@ __global__ void k_prep_nodes(TnDev d)
     if (s >= d.n) return;
     const int i = d.order ? d.order[s] : s;
     d.zs[s] = d.species[i];
-    const int b = d.batch[s];  // batch is in original order; s doubles as an original index here
-    if (s == 0 || d.batch[s - 1] != b) d.sample_ptr[b] = s;
-    if (s == d.n - 1) d.sample_ptr[d.n_samples] = d.n;
+    // sample_ptr[b] = first atom of sample b (batch is non-decreasing, original order; s doubles as an
+    // original index here).  Every entry is written exactly once: the codes (prev, b] start at s
+    // (empty samples in between included), the codes past the last atom's end at n.
+    const int b = d.batch[s];
+    const int prev = s == 0 ? -1 : d.batch[s - 1];
+    for (int c = prev + 1; c <= b; ++c) d.sample_ptr[c] = s;
+    if (s == d.n - 1)
+        for (int c = b + 1; c <= d.n_samples; ++c) d.sample_ptr[c] = d.n;
 }
 
 // Per-edge geometry shared by every layer of the forward and reverse sweeps, written in the
@@ -783,18 +788,26 @@ __global__ void __launch_bounds__(256) k_readout_feats(TnDev d, const float *X)
     }
 }
 
-// per-atom energy: (silu(r1) . h2_w + h2_b) * std + mean  (graphnet.py:403-406), original order
+// per-atom energy: (silu(r1) . h2_w + h2_b) * std + mean  (graphnet.py:403-406), original order;
+// also the head's own reverse (g_r1) and the caller's per-atom copy
 __global__ void k_head(TnDev d, int H)
 {
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= d.n) return;
     float part = 0.0f;
-    for (int h = lane; h < H; h += 32) part += nnp_silu(d.r1[(size_t)s * H + h]) * d.m.h2_w[h];
+    for (int h = lane; h < H; h += 32) {
+        const float r = d.r1[(size_t)s * H + h], w = d.m.h2_w[h];
+        part += nnp_silu(r) * w;
+        // reverse of this very line: dE/dr1 = std * h2_w * silu'(r1)  (energy-only calls ignore it)
+        d.g_r1[(size_t)s * H + h] = d.m.std * w * nnp_silu_grad(r);
+    }
     part = nnp_warp_sum(part);
     if (lane == 0) {
         const float e = (part + d.m.h2_b) * d.m.std + d.m.mean;
-        d.e_atom[d.order ? d.order[s] : s] = e;
+        const int i = d.order ? d.order[s] : s;
+        d.e_atom[i] = e;
+        if (d.per_atom) d.per_atom[i] = e;
     }
 }
 
@@ -814,20 +827,6 @@ __global__ void __launch_bounds__(1024) k_energy_sum(TnDev d)
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
         d.energy[b] = (float)t;
     }
-}
-
-__global__ void k_copy_per_atom(TnDev d)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < d.n) d.per_atom[i] = d.e_atom[i];
-}
-
-__global__ void k_head_bwd(TnDev d, int H)
-{
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= d.n * H) return;
-    const int h = idx % H;
-    d.g_r1[idx] = d.m.std * d.m.h2_w[h] * nnp_silu_grad(d.r1[idx]);
 }
 
 // reverse of k_readout_feats: GX = 2 * g_feats[grp] * X_part
@@ -1098,12 +1097,6 @@ __global__ void __launch_bounds__(256) k_forces(TnDev d)
     }
 }
 
-__global__ void k_fill_int(int *p, int n, int v)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
-}
-
 // --------------------------------------------------------------------------------- host side
 size_t carve(TnDev &d, void *ws)
 {
@@ -1265,7 +1258,6 @@ int run_step(TnDev &d, cudaStream_t st)
         if (rc) return rc; \
     } while (0)
 
-    { NNP_PROF("k_fill_int", st); k_fill_int<<<NNP_GRID(nnp_blocks(d.n_samples + 1, 256)), 256, 0, st>>>(d.sample_ptr, d.n_samples + 1, n); }
     { NNP_PROF("k_prep_nodes", st); k_prep_nodes<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d); }
     { NNP_PROF("k_edge_order", st); k_edge_order<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     { NNP_PROF("k_edge_rev", st); k_edge_rev<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
@@ -1314,12 +1306,10 @@ int run_step(TnDev &d, cudaStream_t st)
     }
     { NNP_PROF("k_head", st); k_head<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, H); }
     { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), (n / d.n_samples >= 2048 ? 1024 : 256), 0, st>>>(d); }
-    if (d.per_atom) k_copy_per_atom<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d);
     NNP_CHECK_LAUNCH("tensornet forward");
     if (!d.forces) return NNP_OK;
 
     // ================================================================= reverse sweep
-    { NNP_PROF("k_head_bwd", st); k_head_bwd<<<NNP_GRID(nnp_blocks((int64_t)n * H, 256)), 256, 0, st>>>(d, H); }
     {
         GemmBatch b{};
         // g_r0 = (g_r1 @ h1_w) * silu'(r0)
