@@ -154,6 +154,18 @@ typedef struct nnp_tn_model {
     nnp_gemm_weight h1_w, h1_wT;                        /* [C/2,C], [C,C/2] */
     const float *lin_b, *h1_b;                          /* [C], [C/2] */
     const float *h2_w;                                  /* [C/2] */
+    /* Embedding reverse by node-level projection (optional; embed_projection = 0 keeps the
+       per-channel edge kernel).  The distance projections are linear in the expnorm basis,
+       dp_j(rho)[c] = sum_k dp_wT[j][k][c] rho_k + dp_b[j][c], so dE/dX0 is first contracted over
+       channels per node (two tcgen05 GEMMs against species-weighted copies of dp_wT, built on the
+       device from the species present in the step) and every edge then costs 9 x num_rbf
+       multiply-adds instead of ~60 per channel.  Needs num_rbf == 32; steps with more than four
+       species fall back to the per-channel kernel on the device. */
+    int32_t embed_projection;
+    int32_t reserved0;
+    const float *dp_wT;                                 /* [3][num_rbf][C] */
+    const float *dp_b;                                  /* [3][C] */
+    const float *rbf_means, *rbf_betas;                 /* [num_rbf] (radial.py:62-73) */
 } nnp_tn_model;
 
 int nnp_tn_workspace_bytes(const nnp_tn_model *m, int32_t n_atoms, int32_t capacity,

@@ -87,7 +87,17 @@ struct TnDev {
     float *Qc, *lnr, *r0, *sr0, *r1, *e_atom;
     float *G1, *G2, *G3;  // [N,9,C] gradient scratch
     float *g_r1, *g_r0, *g_lnr, *g_e1, *g_e0, *g_ln0;
+    // embedding reverse by node-level projection (NULL when the model does not ask for it)
+    int *present;       // [max_z] species seen this step
+    int *slot_of_z;     // [max_z] slot (0..3) of a present species, in increasing species order
+    int *slot_species;  // [EMB_SLOTS] species of a slot, -1 when unused
+    int *embed_fast;    // [1] 1 = this step has at most EMB_SLOTS species: the projected kernels run
+    float *Wproj;       // [3 groups][sender | receiver][EMB_SLOTS * 32][C] species-weighted dp weights
+    float *Hb;          // [N][EMB_SLOTS * 9] bias column of the projection
 };
+
+constexpr int EMB_SLOTS = 4;   // species slots of the projected embedding reverse (EMB_SLOTS * 32 = 128 GEMM columns)
+constexpr int EMB_K = 32;      // radial basis size it is written for
 
 __device__ __forceinline__ bool overflowed(const TnDev &d)
 {
@@ -98,6 +108,8 @@ __device__ __forceinline__ bool overflowed(const TnDev &d)
 __global__ void k_prep_nodes(TnDev d)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d.present)
+        for (int z = s; z < d.m.max_z; z += gridDim.x * blockDim.x) d.present[z] = 0;
     if (s >= d.n) return;
     const int i = d.order ? d.order[s] : s;
     d.zs[s] = d.species[i];
@@ -125,6 +137,7 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
     if (s >= d.n) return;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
     const float rl = d.m.cutoff_lower, ru = d.m.cutoff_upper;
+    if (d.present && lane == 0) d.present[d.zs[s]] = 1;   // (same value from every writer)
     for (int e = e0 + lane; e < e1; e += 32) {
         const float dist = d.dists[e];
         int rank = 0;
@@ -235,6 +248,48 @@ __device__ __forceinline__ void table_lookup_group(const float *__restrict__ tab
 }
 
 __device__ __forceinline__ int group_of(int q) { return q == 0 ? 0 : (q < 4 ? 1 : 2); }
+
+// Species slots of the projected embedding reverse.  Every block recomputes the slot table from the
+// species marked present (increasing species order; at most EMB_SLOTS, else the step falls back to
+// the per-channel kernel), block 0 publishes it, and block (group, side, slot) writes its 32 rows of
+//   Wproj[group][side][slot * 32 + k][c] = ztab_side[species(slot)][c] * dp_wT[group][k][c]
+// (side 0: sender table z_send, side 1: receiver table z_recv), the GEMM weights that contract
+// dE/dX0 over channels for every (species, radial basis function).
+__global__ void __launch_bounds__(256) k_embed_slots(TnDev d)
+{
+    __shared__ int sp[EMB_SLOTS];
+    const int C = d.m.channels;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (lane < EMB_SLOTS) sp[lane] = -1;
+        __syncwarp();
+        int count = 0;
+        for (int base = 0; base < d.m.max_z; base += 32) {
+            const int z = base + lane;
+            const bool p = z < d.m.max_z && d.present[z] != 0;
+            const unsigned b = __ballot_sync(NNP_FULL_MASK, p);
+            const int slot = count + __popc(b & ((1u << lane) - 1u));
+            if (p && slot < EMB_SLOTS) sp[slot] = z;
+            if (blockIdx.x == 0 && z < d.m.max_z) d.slot_of_z[z] = (p && slot < EMB_SLOTS) ? slot : 0;
+            count += __popc(b);
+        }
+        __syncwarp();
+        if (blockIdx.x == 0) {
+            if (lane < EMB_SLOTS) d.slot_species[lane] = sp[lane];
+            if (lane == 0) d.embed_fast[0] = count <= EMB_SLOTS ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    const int slot = blockIdx.x % EMB_SLOTS, side = (blockIdx.x / EMB_SLOTS) & 1, grp = blockIdx.x / (2 * EMB_SLOTS);
+    const int z = sp[slot];
+    const float *ztab = (side ? d.m.z_recv : d.m.z_send) + (size_t)(z < 0 ? 0 : z) * C;
+    const float *w = d.m.dp_wT + (size_t)grp * EMB_K * C;
+    float *out = d.Wproj + ((size_t)(grp * 2 + side) * EMB_SLOTS + slot) * EMB_K * C;
+    for (int idx = threadIdx.x; idx < EMB_K * C; idx += blockDim.x) {
+        const int c = idx % C;
+        out[idx] = z < 0 ? 0.0f : ztab[c] * w[idx];
+    }
+}
 
 // ----------------------------------------------------------------------------- embedding
 // X0_i = sum_e w_e[:,grp] * basis_e  with w_e = dp(rho_e) * phi_e * Z_e ; then n0 = |X0|^2 and
@@ -932,15 +987,63 @@ __global__ void __launch_bounds__(256) k_embed_norm_bwd(TnDev d, float *GX0)
     for (int v = 0; v < CPL; ++v) gn[v] = rstd * (gxh[v] - s1 - xh[v] * s2);
     const float *x0 = d.X0 + (size_t)s * 9 * C + cb;
     float *out = GX0 + (size_t)s * 9 * C + cb;
+    float t[9][CPL];
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
-        float x[CPL], o[CPL];
+        float x[CPL];
         ldv<CPL>(x0 + q * C, x);
-        ldv<CPL>(out + q * C, o);
+        ldv<CPL>(out + q * C, t[q]);
 #pragma unroll
-        for (int v = 0; v < CPL; ++v) o[v] += 2.0f * gn[v] * x[v];
-        stv<CPL>(out + q * C, o);
+        for (int v = 0; v < CPL; ++v) t[q][v] += 2.0f * gn[v] * x[v];
+        stv<CPL>(out + q * C, t[q]);
     }
+    if (!d.Hb) return;
+    // bias column of the projected embedding reverse:
+    //   Hb[s][slot][q] = sum_c (z_recv[z_s][c] + z_send[species(slot)][c]) dp_b[grp(q)][c] G[q][c]
+    float zr[CPL], part[EMB_SLOTS * 9];
+    ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float b[CPL];
+        ldv<CPL>(d.m.dp_b + k * C + cb, b);
+#pragma unroll
+        for (int q = (k == 0 ? 0 : (k == 1 ? 1 : 4)); q < (k == 0 ? 1 : (k == 1 ? 4 : 9)); ++q)
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) t[q][v] *= b[v];
+    }
+#pragma unroll
+    for (int sl = 0; sl < EMB_SLOTS; ++sl) {
+        const int z = d.slot_species[sl];
+        float zz[CPL];
+        ldv<CPL>(d.m.z_send + (size_t)(z < 0 ? 0 : z) * C + cb, zz);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            float a = 0.0f;
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) a = fmaf(zr[v] + zz[v], t[q][v], a);
+            part[sl * 9 + q] = a;
+        }
+    }
+    // 36 warp sums: the first 32 by a transposing butterfly (31 shuffles; lane l ends up with the
+    // total of value l), the last four one by one
+    float tail[EMB_SLOTS * 9 - 32];
+#pragma unroll
+    for (int i = 32; i < EMB_SLOTS * 9; ++i) tail[i - 32] = nnp_warp_sum(part[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const float send = up ? part[i] : part[i + o];
+            const float keep = up ? part[i + o] : part[i];
+            part[i] = keep + __shfl_xor_sync(NNP_FULL_MASK, send, o);
+        }
+    }
+    float *hb = d.Hb + (size_t)s * (EMB_SLOTS * 9);
+    hb[lane] = part[0];
+#pragma unroll
+    for (int i = 32; i < EMB_SLOTS * 9; ++i)
+        if (lane == i - 32) hb[i] = tail[i - 32];
 }
 
 // reverse of k_embed_edge: per edge g_d += dE/dd (through dp(rho) and phi) and g_u = dE/du
@@ -949,6 +1052,7 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
 {
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
+    if (d.embed_fast && d.embed_fast[0]) return;   // the projected kernels do this step's embedding reverse
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int s = gw / NPARTS, part = gw - s * NPARTS;
@@ -1051,6 +1155,106 @@ __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX
     }
 }
 
+// Reverse of k_embed_edge through the node-level projection.  Hs[i][q][slot*32+k] and
+// Hr[i][q][slot*32+k] are dE/dX0 contracted over channels against z_send[species(slot)] * dp_w and
+// z_recv[species(slot)] * dp_w (two channel-mix shaped GEMMs); with
+//   Hc[slot][q][k] = Hs[i][q][slot][k] + Hr[i][q][slot(z_i)][k],   chi_k = phi rho_k,   psi_k = d(phi rho_k)/dd
+// an edge e = (i <- j), slot = slot(z_j), gives
+//   dE/dd_e = sum_k psi_k (3 Hc[0] + sum_{q in A} 2 u_q Hc[q] + sum_{q in S} s_q Hc[q])[k]
+//   dE/du_e = 2 sum_k chi_k (Hc[1..3] + sym(Hc[4..8]) u)[k]
+// plus the bias column (chi = phi, psi = phi') from Hb.  One warp per receiver stages Hc in shared
+// memory, then every lane owns one edge of the row: no reductions, coalesced stores.
+// rho_k = exp(-beta_k (u - mu_k)^2), u = exp(cutoff_lower - d)  (radial.py:53-59).
+constexpr int EMB_PROJ_WARPS = 4;
+constexpr int EMB_PROJ_STRIDE = 9 * EMB_K + 4;   // slot stride: slots land on different banks
+__global__ void __launch_bounds__(EMB_PROJ_WARPS * 32) k_embed_edge_bwd_proj(TnDev d, const float *Hs,
+                                                                             const float *Hr)
+{
+    __shared__ __align__(16) float hc_all[EMB_PROJ_WARPS][EMB_SLOTS * EMB_PROJ_STRIDE];
+    __shared__ __align__(16) float hb_all[EMB_PROJ_WARPS][EMB_SLOTS * 9 + 4];
+    __shared__ __align__(16) float mu_s[EMB_K], beta_s[EMB_K];
+    if (threadIdx.x < EMB_K) {
+        mu_s[threadIdx.x] = d.m.rbf_means[threadIdx.x];
+        beta_s[threadIdx.x] = d.m.rbf_betas[threadIdx.x];
+    }
+    __syncthreads();
+    if (overflowed(d) || !d.embed_fast[0]) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s = blockIdx.x * EMB_PROJ_WARPS + warp;
+    if (s >= d.n) return;
+    float *hc = hc_all[warp], *hb = hb_all[warp];
+    {
+        const int my = d.slot_of_z[d.zs[s]];
+        const float *ps = Hs + (size_t)s * 9 * (EMB_SLOTS * EMB_K) + lane;
+        const float *pr = Hr + (size_t)s * 9 * (EMB_SLOTS * EMB_K) + my * EMB_K + lane;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            const float r = pr[q * (EMB_SLOTS * EMB_K)];
+#pragma unroll
+            for (int sl = 0; sl < EMB_SLOTS; ++sl)
+                hc[sl * EMB_PROJ_STRIDE + q * EMB_K + lane] = ps[q * (EMB_SLOTS * EMB_K) + sl * EMB_K] + r;
+        }
+        const float *pb = d.Hb + (size_t)s * (EMB_SLOTS * 9);
+        hb[lane] = pb[lane];
+        if (lane < EMB_SLOTS * 9 - 32) hb[32 + lane] = pb[32 + lane];
+    }
+    __syncwarp();
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    for (int e = e0 + lane; e < e1; e += 32) {
+        const int j = d.col[e];
+        if (j == s) continue;                       // a self loop has no geometry
+        const int sl = d.slot_of_z[d.zs[j]];
+        const float4 ga = d.geoA[e];
+        const float4 gb = d.geoB[e];
+        const float u = gb.w, phi = ga.y, dphi = ga.z;
+        const float c1 = 2.0f * u * phi;            // psi_k = rho_k (c1 beta_k (u - mu_k) + phi')
+        float hp[9], hx[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) hp[q] = hx[q] = 0.0f;
+        const float4 *H4 = reinterpret_cast<const float4 *>(hc + sl * EMB_PROJ_STRIDE);
+#pragma unroll 2
+        for (int k4 = 0; k4 < EMB_K / 4; ++k4) {
+            const float4 mu = reinterpret_cast<const float4 *>(mu_s)[k4];
+            const float4 be = reinterpret_cast<const float4 *>(beta_s)[k4];
+            float chi[4], psi[4];
+            {
+                const float m4[4] = {mu.x, mu.y, mu.z, mu.w}, b4[4] = {be.x, be.y, be.z, be.w};
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float df = u - m4[v];
+                    const float t = b4[v] * df;
+                    const float rho = __expf(-t * df);
+                    chi[v] = rho * phi;
+                    psi[v] = rho * fmaf(c1, t, dphi);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float4 h = H4[q * (EMB_K / 4) + k4];
+                hp[q] = fmaf(psi[0], h.x, fmaf(psi[1], h.y, fmaf(psi[2], h.z, fmaf(psi[3], h.w, hp[q]))));
+                if (q > 0)
+                    hx[q] = fmaf(chi[0], h.x, fmaf(chi[1], h.y, fmaf(chi[2], h.z, fmaf(chi[3], h.w, hx[q]))));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            const float b = hb[sl * 9 + q];
+            hp[q] = fmaf(dphi, b, hp[q]);
+            hx[q] = fmaf(phi, b, hx[q]);
+        }
+        const float uu = (gb.x * gb.x + gb.y * gb.y + gb.z * gb.z) * (1.0f / 3.0f);
+        const float b4 = gb.x * gb.x - uu, b5 = gb.y * gb.y - uu;
+        const float a1 = 2.0f * gb.x, a2 = 2.0f * gb.y, a3 = 2.0f * gb.z;
+        const float pd = 3.0f * hp[0] + a1 * hp[1] + a2 * hp[2] + a3 * hp[3] + (2.0f * b4 + b5) * hp[4] +
+                         (2.0f * b5 + b4) * hp[5] + a1 * gb.y * hp[6] + a1 * gb.z * hp[7] + a2 * gb.z * hp[8];
+        const float px = hx[1] + hx[4] * gb.x + hx[6] * gb.y + hx[7] * gb.z;
+        const float py = hx[2] + hx[6] * gb.x + hx[5] * gb.y + hx[8] * gb.z;
+        const float pz = hx[3] + hx[7] * gb.x + hx[8] * gb.y - (hx[4] + hx[5]) * gb.z;
+        d.g_d[e] = pd;                              // slot 0 of the embedding's share
+        d.g_u[e] = make_float4(2.0f * px, 2.0f * py, 2.0f * pz, 0.0f);
+    }
+}
+
 // forces: F_i = -sum_{e in row i} [ (g_d[e] + g_d[e']) u_e + (1 - u u^T)(g_u[e] - g_u[e']) / d_e ]
 // with e' the reverse edge (u_e' = -u_e), precomputed by k_edge_rev.  One warp per atom: lanes
 // take the row's edges 32 at a time (every edge costs a few dependent scattered reads), then a
@@ -1144,6 +1348,14 @@ size_t carve(TnDev &d, void *ws)
     d.g_e1 = ar.take<float>(n * 3 * C);
     d.g_e0 = ar.take<float>(n * 2 * C);
     d.g_ln0 = ar.take<float>(n * C);
+    if (d.m.embed_projection) {
+        d.present = ar.take<int>((size_t)d.m.max_z);
+        d.slot_of_z = ar.take<int>((size_t)d.m.max_z);
+        d.slot_species = ar.take<int>(EMB_SLOTS);
+        d.embed_fast = ar.take<int>(1);
+        d.Wproj = ar.take<float>((size_t)3 * 2 * EMB_SLOTS * EMB_K * C);
+        d.Hb = ar.take<float>(n * EMB_SLOTS * 9);
+    }
     return ar.bytes();
 }
 
@@ -1156,6 +1368,9 @@ int validate_model(const nnp_tn_model *m)
     NNP_CHECK_ARG(m->num_knots >= 2, "num_knots must be >= 2");
     NNP_CHECK_ARG(m->u_step > 0.0f, "u_step must be positive");
     NNP_CHECK_ARG(m->cutoff_lower >= 0.0f && m->cutoff_lower < m->cutoff_upper, "bad cutoffs");
+    NNP_CHECK_ARG(!m->embed_projection || (m->num_rbf == EMB_K && m->channels == EMB_SLOTS * EMB_K && m->dp_wT && m->dp_b && m->rbf_means &&
+                                           m->rbf_betas && m->max_z >= 1),
+                  "embed_projection needs num_rbf == 32, 128 channels and the dp / rbf arrays");
     return NNP_OK;
 }
 
@@ -1261,6 +1476,7 @@ int run_step(TnDev &d, cudaStream_t st)
     { NNP_PROF("k_prep_nodes", st); k_prep_nodes<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d); }
     { NNP_PROF("k_edge_order", st); k_edge_order<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     { NNP_PROF("k_edge_rev", st); k_edge_rev<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
+    if (d.m.embed_projection && d.forces) { NNP_PROF("k_embed_slots", st); k_embed_slots<<<NNP_GRID(3 * 2 * EMB_SLOTS), 256, 0, st>>>(d); }
 
     // ---- embedding
     { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d))); }
@@ -1348,6 +1564,23 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
     { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
+    if (d.m.embed_projection) {
+        // Hs = G_X0 against the sender-species weights, Hr against the receiver-species weights
+        // (Ga and GX are free by now); then one lane per edge
+        nnp_gemm_weight ws[3], wr[3];
+        for (int k = 0; k < 3; ++k) {
+            ws[k].w = d.Wproj + (size_t)(k * 2 + 0) * EMB_SLOTS * EMB_K * C;
+            wr[k].w = d.Wproj + (size_t)(k * 2 + 1) * EMB_SLOTS * EMB_K * C;
+        }
+        GemmBatch ms = mix_gemm(Gb, ws, Ga, n, C), mr = mix_gemm(Gb, wr, GX, n, C);
+        for (int k = 0; k < 3; ++k) {
+            ms.g[k].N = mr.g[k].N = EMB_SLOTS * EMB_K;
+            ms.g[k].ldo = mr.g[k].ldo = EMB_SLOTS * EMB_K;
+        }
+        { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(ms, 3, st))); }
+        { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mr, 3, st))); }
+        { NNP_PROF("k_embed_edge_bwd_proj", st); k_embed_edge_bwd_proj<<<NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st>>>(d, Ga, GX); }
+    }
     { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d, Gb))); }
     { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
     NNP_CHECK_LAUNCH("tensornet reverse");

@@ -18,6 +18,7 @@ neighbor structure is detected after the step and answered like ``build_with_aut
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, replace
 from typing import Dict, Optional
 
@@ -192,7 +193,7 @@ class TensorNet:
 
     def __init__(self, config: Optional[TNConfig] = None, params: Optional[Dict[str, np.ndarray]] = None,
                  seed: int = 0, device="cuda", use_graph: bool = True, strategy: str = "auto",
-                 **config_kwargs):
+                 embed_projection: Optional[bool] = None, **config_kwargs):
         torch = _lib.require_cuda()
         self._torch = torch
         self.lib = _lib.load()
@@ -205,6 +206,7 @@ class TensorNet:
         self.device = torch.device(device)
         self.use_graph = use_graph
         self.strategy = strategy
+        self.embed_projection = embed_projection
         self._plans: Dict[tuple, _Plan] = {}
         self._capacity_hint: Dict[tuple, int] = {}
         self._upload()
@@ -258,6 +260,15 @@ class TensorNet:
         gemm_weight(m.h1_wT, "h1_wT", P["h1_w"].T)
         m.lin_b, m.h1_b = dev("lin_b", P["lin_b"]), dev("h1_b", P["h1_b"])
         m.h2_w = dev("h2_w", P["h2_w"])
+        # embedding reverse by node-level projection (written for 128 channels and 32 basis functions;
+        # other shapes keep the per-channel edge kernel)
+        want = self.embed_projection
+        if want is None:
+            want = os.environ.get("NNP_EMBED_PROJ", "1") != "0"
+        m.embed_projection = int(bool(want) and C == 128 and cfg.num_rbf == 32)
+        m.dp_wT = dev("dp_wT", np.transpose(P["dp_w"], (0, 2, 1)))      # [3][K][C]
+        m.dp_b = dev("dp_b", P["dp_b"])
+        m.rbf_means, m.rbf_betas = dev("rbf_means", P["rbf_means"]), dev("rbf_betas", P["rbf_betas"])
         self._model = m
         self._weights = keep
 

@@ -312,3 +312,67 @@ def test_config_e_full_size_properties():
     e3, f3 = model(zt, torch.as_tensor(shifted), None, box)
     assert abs(float(e3[0] - e1[0])) / abs(float(e1[0])) < 2e-6
     assert float((f3 - f1).abs().max() / f1.abs().max()) < 2e-4   # float32 positions move by ~1e-6 A
+
+
+# ---------------------------------------------------------------- projected embedding reverse
+def _cloud22(seed):
+    """Config A's 22-point cloud (0.9 A minimum separation) for another seed."""
+    return synth.config_a_molecule(seed)[1]
+
+
+def _both_embed_paths(z, pos, batch, box, **kw):
+    """Forces from the node-projected embedding reverse and from the per-channel edge kernel."""
+    out = []
+    for proj in (True, False):
+        model = P.TensorNet(embedding_dimension=128, num_rbf=32, embed_projection=proj, **kw)
+        assert bool(model._model.embed_projection) == proj
+        e, f = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32),
+                     None if batch is None else torch.as_tensor(batch), box)
+        out.append((model, e.cpu().numpy(), f.cpu().numpy()))
+    return out
+
+
+@pytest.mark.parametrize("L", [0, 2])
+@pytest.mark.parametrize("species", [[7], [1, 6, 8], [1, 35, 60, 99], [1, 6, 7, 8, 9], [2, 3, 5, 7, 11, 13, 17, 19, 23]])
+def test_embed_projection_matches_oracle_and_edge_kernel(rng, L, species):
+    """1-4 species run the projected kernels, 5 and 9 species fall back on the device; both must
+    agree with the oracle and with each other (sparse species codes up to max_z - 1 included)."""
+    n = 22
+    pos = _cloud22(5)
+    z = rng.choice(species, n)
+    z[: len(species)] = species
+    (mp, ep, fp), (mo, eo, fo) = _both_embed_paths(z, pos, None, None, num_layers=L, cutoff_upper=5.0,
+                                                   max_z=100, seed=0)
+    check(mp, z, pos, None, None)
+    check(mo, z, pos, None, None)
+    assert np.array_equal(ep, eo)                      # the forward sweep is the same code
+    assert np.max(np.abs(fp - fo)) / np.max(np.abs(fo)) < 2e-5
+
+
+def test_embed_projection_lower_cutoff_triclinic_and_batches(rng):
+    box = np.array([[11.0, 0, 0], [2.5, 10.5, 0], [-3.0, 1.5, 12.0]])
+    pos = (rng.uniform(0, 1, (90, 3)) @ box).astype(np.float32).astype(np.float64)
+    z = rng.choice([1, 6, 8], 90)
+    (mp, ep, fp), (mo, eo, fo) = _both_embed_paths(z, pos, None, box, num_layers=1, cutoff_lower=0.7,
+                                                   cutoff_upper=4.5, max_z=10, seed=6)
+    check(mp, z, pos, None, box)
+    assert np.max(np.abs(fp - fo)) / np.max(np.abs(fo)) < 2e-5
+    z, pos, batch, _ = synth.config_d_molecules(48, seed=8)
+    z = np.where(z == 9, 8, z)                         # four species: the projected kernels run
+    (mp, ep, fp), (mo, eo, fo) = _both_embed_paths(z, pos, batch, None, num_layers=2, cutoff_upper=5.0, seed=2)
+    check(mp, z, pos, batch, None)
+    assert np.max(np.abs(fp - fo)) / np.max(np.abs(fo)) < 2e-5
+
+
+def test_embed_projection_species_set_changes_between_replays(rng):
+    """The slot table and the species-weighted GEMM weights are rebuilt on the device every step, so
+    one captured graph serves inputs with different species sets (and falls back when they exceed
+    four)."""
+    n = 22
+    pos = _cloud22(6)
+    model = P.TensorNet(embedding_dimension=128, num_layers=1, num_rbf=32, cutoff_upper=5.0, max_z=20, seed=3)
+    for species in ([1, 8], [6, 7, 8, 9], [1, 2, 3, 4, 5, 6], [14]):
+        z = rng.choice(species, n)
+        z[: len(species)] = species
+        check(model, z, pos, None, None)
+    assert len(model._plans) == 1
