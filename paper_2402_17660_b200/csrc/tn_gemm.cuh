@@ -243,9 +243,16 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
                 for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
                     for (int ni = 0; ni < 2; ++ni) {
-                        mma_tf32(acc[mi][ni], al[mi], bh[ni]);
-                        mma_tf32(acc[mi][ni], ah[mi], bl[ni]);
-                        mma_tf32(acc[mi][ni], ah[mi], bh[ni]);
+                        // The tensor core adds into its accumulator with truncation: chaining all K
+                        // steps inside it shrinks every output by ~1e-6 relative (measured: a
+                        // systematic 5e-6 energy error).  Each K step therefore starts from zero and
+                        // is added to the running sum by an ordinary round-to-nearest FADD.
+                        float t[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                        mma_tf32(t, al[mi], bh[ni]);
+                        mma_tf32(t, ah[mi], bl[ni]);
+                        mma_tf32(t, ah[mi], bh[ni]);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[mi][ni][q] += t[q];
                     }
             }
         } else {

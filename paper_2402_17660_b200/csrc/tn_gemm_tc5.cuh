@@ -130,7 +130,13 @@ __device__ __forceinline__ void split_store(char *hi_base, char *lo_base, uint32
 template <int PRO, int EPI, int NT>
 __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
 {
-    constexpr int TMEM_COLS = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
+    // The tensor core adds into a TMEM accumulator with truncation, which shrinks a long chain of
+    // K steps by ~1e-6 relative (measured as a systematic energy error).  Each K chunk therefore
+    // gets a fresh accumulator (two of them, used alternately) whose 12 MMAs add the small
+    // correction terms first, and the chunks are summed in registers by round-to-nearest FADDs
+    // while the next chunk's MMAs run.
+    constexpr int ACC_COLS = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
+    constexpr int TMEM_COLS = 2 * ACC_COLS;
     constexpr int A_PASSES = BM / 16;   // 128 threads cover 16 rows x 8 chunks per pass
     constexpr int W_PASSES = NT / 16;
     const GemmArgs &g = batch.g[blockIdx.z];
@@ -198,6 +204,20 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     const uint64_t da_hi = make_desc(smem_u32(a_hi)), da_lo = make_desc(smem_u32(a_lo));
     const uint64_t dw_hi = make_desc(smem_u32(w_hi)), dw_lo = make_desc(smem_u32(w_lo));
 
+    float acc[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) acc[i] = 0.0f;
+    // thread (warp, lane) owns accumulator lane 32*warp + lane = one output row
+    auto drain = [&](int buf) {
+#pragma unroll
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem_d + (uint32_t)(buf * ACC_COLS) + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
+        }
+    };
+
     load_chunk(0);
     for (int c = 0; c < nchunks; ++c) {
         if (c > 0) {
@@ -223,19 +243,26 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dst = tmem_d + (uint32_t)((c & 1) * ACC_COLS);
 #pragma unroll
             for (int ks = 0; ks < KC / 8; ++ks) {
                 const uint64_t adv = (uint64_t)(ks * 32 >> 4);   // 8 tf32 = 32 bytes along K
-                umma_tf32(tmem_d, da_lo + adv, dw_hi + adv, idesc, (c | ks) != 0);
-                umma_tf32(tmem_d, da_hi + adv, dw_lo + adv, idesc, 1);
-                umma_tf32(tmem_d, da_hi + adv, dw_hi + adv, idesc, 1);
+                umma_tf32(dst, da_lo + adv, dw_hi + adv, idesc, ks != 0);
+                umma_tf32(dst, da_hi + adv, dw_lo + adv, idesc, 1);
+            }
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+                const uint64_t adv = (uint64_t)(ks * 32 >> 4);
+                umma_tf32(dst, da_hi + adv, dw_hi + adv, idesc, 1);
             }
             umma_commit(&mma_bar);
         }
         if (c + 1 < nchunks) load_chunk(c + 1);             // overlaps the MMAs just issued
+        if (c > 0) drain((c - 1) & 1);                       // chunk c-1 is complete (waited for above)
     }
     mbar_wait(&mma_bar, (uint32_t)((nchunks - 1) & 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    drain((nchunks - 1) & 1);
 
     // epilogue, phase 1: TMEM -> registers -> shared memory.  Thread (warp, lane) owns accumulator
     // lane 32*warp + lane = one output row; the operand buffers are free now and are reused as a
@@ -245,15 +272,13 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     float *stage = reinterpret_cast<float *>(smem);
     {
         const int rr = warp * 32 + lane;
-#pragma unroll 1
+#pragma unroll
         for (int c0 = 0; c0 < NT; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int pos = ((c0 >> 2) + q) ^ (rr & (CH - 1));
                 *reinterpret_cast<float4 *>(stage + rr * NT + pos * 4) =
-                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    make_float4(acc[c0 + 4 * q], acc[c0 + 4 * q + 1], acc[c0 + 4 * q + 2], acc[c0 + 4 * q + 3]);
             }
         }
     }
