@@ -53,6 +53,9 @@ typedef void *nnp_stream_t; /* a cudaStream_t */
 
 const char *nnp_last_error(void);
 int nnp_version(void);
+/* sizeof of the ABI structs as this library was compiled (0 = nnp_nl_params, 1 = nnp_tn_model,
+ * 2 = nnp_prior_params; -1 for anything else): lets a binding check its own struct layout. */
+int nnp_abi_sizeof(int which);
 
 /* ------------------------------------------------------------------ neighbor search
  * Replaces build_neighbor_list (neighbors.py:136-235) and the four numba kernels

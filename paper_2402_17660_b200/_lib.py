@@ -24,7 +24,7 @@ NL_FULL_LIST, NL_SELF_LOOPS, NL_RENUMBER, NL_F32_OUT, NL_NO_PAD = 1, 2, 4, 8, 16
 TN_MAX_LAYERS = 8
 
 EXPORTED_SYMBOLS = (
-    "nnp_last_error", "nnp_version", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
+    "nnp_last_error", "nnp_version", "nnp_abi_sizeof", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
     "nnp_distance_pullback", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
     "nnp_test_gemm_nt", "nnp_set_gemm_mode", "nnp_launch_count", "nnp_profile_begin",
     "nnp_profile_report", "nnp_md_langevin_middle", "nnp_priors_pair_terms",

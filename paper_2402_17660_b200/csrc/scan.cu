@@ -89,7 +89,16 @@ extern "C" int nnp_profile_report(char *buf, int buf_bytes)
     }
     return NNP_OK;
 }
-extern "C" int nnp_version(void) { return 100; }
+extern "C" int nnp_version(void) { return 101; }
+extern "C" int nnp_abi_sizeof(int which)
+{
+    switch (which) {
+    case 0: return (int)sizeof(nnp_nl_params);
+    case 1: return (int)sizeof(nnp_tn_model);
+    case 2: return (int)sizeof(nnp_prior_params);
+    default: return -1;
+    }
+}
 
 namespace {
 

@@ -153,9 +153,7 @@ class DeviceIntegrator:
         # one checked float64 step creates (and captures) the plan whose pos64 buffer we own
         model.forward(system.species, system.positions, system.batch if system.n_samples > 1 else None,
                       system.box, n_samples=system.n_samples, check=True, clone=False)
-        cap = model._capacity_hint.get((n, system.n_samples), model.neighbor_capacity(n))
-        self.plan = next(p for k, p in model._plans.items()
-                         if k[0] == n and k[1] == system.n_samples and k[2] == cap and not k[4])
+        self.plan = model._last_plan
         f64 = dict(dtype=torch.float64, device=dev)
         self.vel = torch.as_tensor(np.ascontiguousarray(velocities, dtype=np.float64)).to(dev)
         self.acc_scale = torch.as_tensor(FORCE_TO_ACCELERATION / np.asarray(masses, dtype=np.float64)).to(dev)

@@ -185,7 +185,7 @@ class _Plan:
     """Everything that is fixed for one input shape: buffers, neighbor engine, graph."""
 
     __slots__ = ("key", "n", "n_samples", "capacity", "engine", "workspace", "z", "batch", "pos32",
-                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box", "batch_is_zero")
+                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box", "batch_is_zero", "proj")
 
 
 class TensorNet:
@@ -208,6 +208,7 @@ class TensorNet:
         self.strategy = strategy
         self.embed_projection = embed_projection
         self._plans: Dict[tuple, _Plan] = {}
+        self._last_plan: Optional[_Plan] = None
         self._capacity_hint: Dict[tuple, int] = {}
         self._upload()
 
@@ -262,10 +263,11 @@ class TensorNet:
         m.h2_w = dev("h2_w", P["h2_w"])
         # embedding reverse by node-level projection (written for 128 channels and 32 basis functions;
         # other shapes keep the per-channel edge kernel)
-        want = self.embed_projection
-        if want is None:
-            want = os.environ.get("NNP_EMBED_PROJ", "1") != "0"
-        m.embed_projection = int(bool(want) and C == 128 and cfg.num_rbf == 32)
+        self._proj_capable = (C == 128 and cfg.num_rbf == 32 and self.embed_projection is not False
+                              and os.environ.get("NNP_EMBED_PROJ", "1") != "0")
+        if self.embed_projection and not self._proj_capable:
+            raise ValidationError("embed_projection needs embedding_dimension=128 and num_rbf=32")
+        m.embed_projection = 0          # set per step from the plan (see _use_projection)
         m.dp_wT = dev("dp_wT", np.transpose(P["dp_w"], (0, 2, 1)))      # [3][K][C]
         m.dp_b = dev("dp_b", P["dp_b"])
         m.rbf_means, m.rbf_betas = dev("rbf_means", P["rbf_means"]), dev("rbf_betas", P["rbf_betas"])
@@ -284,10 +286,35 @@ class TensorNet:
         # small samples: all-pairs inside each sample; otherwise the cell list
         return "brute" if n / max(n_samples, 1) < 1024 else "cell"
 
-    def _plan(self, n: int, n_samples: int, box: Optional[Box], capacity: int, pos_is_f32: bool) -> _Plan:
+    PROJECTION_MIN_ATOMS = 4096   # below this the two extra GEMM launches cost more than they save
+    PROJECTION_MAX_SPECIES = 4
+
+    def _use_projection(self, species, n: int, count: bool = True) -> bool:
+        """Whether a step over these species runs the node-projected embedding reverse: forced on
+        by ``embed_projection=True``; otherwise for systems of at least PROJECTION_MIN_ATOMS atoms
+        with at most four distinct species (the device falls back by itself if a projected plan is
+        ever fed more, so this is a cost decision, not a correctness one)."""
+        if not self._proj_capable:
+            return False
+        if self.embed_projection:
+            return True
+        if n < self.PROJECTION_MIN_ATOMS:
+            return False
+        if not count:
+            return True
+        torch = self._torch
+        if isinstance(species, torch.Tensor):
+            if species.is_cuda:
+                return int(torch.unique(species).numel()) <= self.PROJECTION_MAX_SPECIES
+            species = species.numpy()
+        present = np.bincount(np.asarray(species).astype(np.int64, copy=False).ravel(), minlength=1)
+        return int(np.count_nonzero(present)) <= self.PROJECTION_MAX_SPECIES
+
+    def _plan(self, n: int, n_samples: int, box: Optional[Box], capacity: int, pos_is_f32: bool,
+              proj: bool = False) -> _Plan:
         torch, cfg = self._torch, self.config
         box_key = None if box is None else (box.kind, box.vectors.tobytes())
-        key = (n, n_samples, capacity, box_key, pos_is_f32)
+        key = (n, n_samples, capacity, box_key, pos_is_f32, proj)
         plan = self._plans.get(key)
         if plan is not None:
             return plan
@@ -299,10 +326,12 @@ class TensorNet:
         plan = _Plan()
         plan.key, plan.n, plan.n_samples, plan.capacity, plan.box = key, n, n_samples, capacity, box
         plan.notes = notes
+        plan.proj = proj
         plan.engine = NeighborEngine(n, n_samples, capacity, box, cfg.cutoff_lower, cfg.cutoff_upper,
                                      code, dims, max_cells, flags, device=self.device,
                                      want_row_ptr=True, want_order=True)
         need = ctypes.c_size_t(0)
+        self._model.embed_projection = int(proj)
         _lib.check(self.lib.nnp_tn_workspace_bytes(ctypes.byref(self._model), n, capacity, n_samples,
                                                    ctypes.byref(need)), "nnp_tn_workspace_bytes")
         dev = self.device
@@ -327,6 +356,7 @@ class TensorNet:
                                                3 * plan.n, stream), "nnp_f32_to_f64")
         eng = plan.engine
         eng.build(plan.pos64, plan.batch)
+        self._model.embed_projection = int(plan.proj)
         rc = self.lib.nnp_tn_energy_forces(
             ctypes.byref(self._model), plan.n, plan.n_samples, plan.capacity, _lib.ptr(plan.z),
             _lib.ptr(plan.batch), _lib.ptr(eng.order), _lib.ptr(eng.row_ptr), _lib.ptr(eng.pairs),
@@ -390,8 +420,10 @@ class TensorNet:
                 n_samples = int(batch_t[-1]) + 1
         box_obj = self._as_box(box)
         capacity = self._capacity_hint.get((n, n_samples), self.neighbor_capacity(n))
+        proj = self._use_projection(z_t, n, count=check)
         for _ in range(32):
-            plan = self._plan(n, n_samples, box_obj, capacity, pos_t.dtype == torch.float32)
+            plan = self._plan(n, n_samples, box_obj, capacity, pos_t.dtype == torch.float32, proj)
+            self._last_plan = plan
             if check:
                 # species range check on whichever side the codes already live (host tensors: no
                 # device reduction and no extra synchronisation per call)
@@ -430,13 +462,7 @@ class TensorNet:
         graph is captured; ``replay(plan)`` re-runs the whole step (neighbor search included)
         on the resident inputs without touching the host."""
         self.forward(z, pos, batch, box, n_samples=n_samples, check=True, clone=False)
-        n = int(self._torch.as_tensor(pos).shape[0])
-        ns = 1 if batch is None else (n_samples or int(self._torch.as_tensor(batch)[-1]) + 1)
-        cap = self._capacity_hint.get((n, ns), self.neighbor_capacity(n))
-        for key, plan in self._plans.items():
-            if key[0] == n and key[1] == ns and key[2] == cap:
-                return plan
-        raise ValidationError("no plan found for these inputs")
+        return self._last_plan
 
     def replay(self, plan: "_Plan") -> None:
         if plan.graph is not None:
@@ -449,6 +475,9 @@ class TensorNet:
         self._enqueue(plan)
 
     def last_per_atom_energy(self, n: int, n_samples: int = 1):
+        last = self._last_plan
+        if last is not None and last.n == n and last.n_samples == n_samples:
+            return last.per_atom
         for key, plan in self._plans.items():
             if key[0] == n and key[1] == n_samples:
                 return plan.per_atom
@@ -467,8 +496,7 @@ class TensorNet:
         if neighbors is None:
             e, f = self.forward(system.species, system.positions, system.batch, system.box,
                                 n_samples=system.n_samples)
-            plan = self._plans[next(k for k in self._plans if k[0] == system.n_atoms
-                                    and k[1] == system.n_samples)]
+            plan = self._last_plan
             return EnergyForces(e.cpu().numpy(), f.cpu().numpy() if forces else None,
                                 plan.per_atom.cpu().numpy())
         spec = neighbors.spec
@@ -489,6 +517,7 @@ class TensorNet:
         z = torch.as_tensor(np.ascontiguousarray(system.species, dtype=np.int32)).to(dev)
         b = torch.as_tensor(np.ascontiguousarray(system.batch, dtype=np.int32)).to(dev)
         need = ctypes.c_size_t(0)
+        self._model.embed_projection = int(self._use_projection(system.species, n))
         _lib.check(self.lib.nnp_tn_workspace_bytes(ctypes.byref(self._model), n, cap, ns,
                                                    ctypes.byref(need)), "nnp_tn_workspace_bytes")
         ws = torch.empty(need.value, dtype=torch.uint8, device=dev)

@@ -339,9 +339,9 @@ def _both_embed_paths(z, pos, batch, box, **kw):
     out = []
     for proj in (True, False):
         model = P.TensorNet(embedding_dimension=128, num_rbf=32, embed_projection=proj, **kw)
-        assert bool(model._model.embed_projection) == proj
         e, f = model(torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32),
                      None if batch is None else torch.as_tensor(batch), box)
+        assert model._last_plan.proj == proj
         out.append((model, e.cpu().numpy(), f.cpu().numpy()))
     return out
 
@@ -384,9 +384,24 @@ def test_embed_projection_species_set_changes_between_replays(rng):
     four)."""
     n = 22
     pos = _cloud22(6)
-    model = P.TensorNet(embedding_dimension=128, num_layers=1, num_rbf=32, cutoff_upper=5.0, max_z=20, seed=3)
+    model = P.TensorNet(embedding_dimension=128, num_layers=1, num_rbf=32, cutoff_upper=5.0, max_z=20, seed=3,
+                        embed_projection=True)
     for species in ([1, 8], [6, 7, 8, 9], [1, 2, 3, 4, 5, 6], [14]):
         z = rng.choice(species, n)
         z[: len(species)] = species
         check(model, z, pos, None, None)
-    assert len(model._plans) == 1
+    assert len(model._plans) == 1 and model._last_plan.proj
+
+
+def test_embed_projection_is_chosen_by_size_and_species():
+    """Auto mode: projected reverse from 4 096 atoms on when at most four species are present."""
+    model = P.TensorNet(embedding_dimension=128, num_layers=1, num_rbf=32, cutoff_upper=5.0, seed=1)
+    z = np.resize([1, 6, 7, 8], 5000)
+    assert model._use_projection(z, 5000) and model._use_projection(torch.as_tensor(z), 5000)
+    assert model._use_projection(torch.as_tensor(z).cuda(), 5000)
+    assert not model._use_projection(z, 4000)
+    assert not model._use_projection(np.resize([1, 6, 7, 8, 9], 5000), 5000)
+    small = P.TensorNet(embedding_dimension=64, num_layers=1, num_rbf=32, cutoff_upper=5.0, seed=1)
+    assert not small._use_projection(z, 5000)
+    with pytest.raises(P.ValidationError):
+        P.TensorNet(embedding_dimension=64, num_layers=1, num_rbf=32, embed_projection=True)

@@ -24,7 +24,17 @@ def test_header_symbols_are_exported():
     for name in sorted(declared):
         assert hasattr(lib, name), f"{name} declared in nnp_b200.h but not exported"
     assert set(_lib.EXPORTED_SYMBOLS) <= declared
-    assert lib.nnp_version() == 100
+    assert lib.nnp_version() == 101
+
+
+def test_ctypes_struct_layouts_match_the_library():
+    """The ctypes mirrors of the ABI structs have the size the library was compiled with (a field
+    added on one side only would silently shift every later pointer)."""
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    assert lib.nnp_abi_sizeof(0) == ctypes.sizeof(_lib.NlParams)
+    assert lib.nnp_abi_sizeof(1) == ctypes.sizeof(_lib.TnModel)
+    assert lib.nnp_abi_sizeof(2) == ctypes.sizeof(_lib.PriorParams)
+    assert lib.nnp_abi_sizeof(3) == -1
 
 
 def test_workspace_queries_and_validation_run_on_host():
