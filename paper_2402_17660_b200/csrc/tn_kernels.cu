@@ -1433,7 +1433,7 @@ static const EdgeTuning &edge_tuning()
 {
     static const EdgeTuning t = {env_int("NNP_CPL_EMB", 4), env_int("NNP_CPL_FWD", 4),
                                  env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
-                                 std::min(env_int("NNP_BWD_BLOCK", 128), 128), env_int("NNP_FWD_BLOCK", 128), env_int("NNP_EMB_BLOCK", 128)};
+                                 std::min(env_int("NNP_BWD_BLOCK", 64), 128), env_int("NNP_FWD_BLOCK", 64), env_int("NNP_EMB_BLOCK", 128)};
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
