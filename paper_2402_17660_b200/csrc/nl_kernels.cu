@@ -60,6 +60,7 @@ struct NlArgs {
     int *cell_id, *cell_start, *cell_cursor, *tmp_order, *sidx, *rank_of, *sbatch, *row_count;
     int *sample_ptr, *scratch_col, *scratch_t, *stage_t;
     double *spos;
+    float4 *slpos;   // cell strategy: (position relative to the atom's own cell corner, original index)
     double *bounds_partial;
     GridDev *grid;
     // outputs
@@ -247,6 +248,32 @@ __global__ void k_cell_rank(NlArgs a)
     a.spos[3 * (size_t)s] = a.pos[3 * (size_t)i];
     a.spos[3 * (size_t)s + 1] = a.pos[3 * (size_t)i + 1];
     a.spos[3 * (size_t)s + 2] = a.pos[3 * (size_t)i + 2];
+    // Single-precision position relative to the corner of the atom's own cell (computed in float64,
+    // so its error is 2^-24 of a cell edge whatever the size of the box); the row scan's prefilter
+    // rebuilds the displacement to a candidate in an adjacent cell as
+    //   (local_a - local_b) - (cell offset) . (cell vectors).
+    const GridDev g = *a.grid;
+    const double x = a.pos[3 * (size_t)i], y = a.pos[3 * (size_t)i + 1], z = a.pos[3 * (size_t)i + 2];
+    const int cc[3] = {c / (g.dims[1] * g.dims[2]), (c / g.dims[2]) % g.dims[1], c % g.dims[2]};
+    double lx, ly, lz;
+    if (a.periodic) {
+        double w[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double f = x * a.inv_box[k] + y * a.inv_box[3 + k] + z * a.inv_box[6 + k];
+            f -= floor(f);
+            w[k] = (f * g.dims[k] - cc[k]) / g.dims[k];     // fraction of the box edge past the cell corner
+        }
+        const Metric &m = a.metric;
+        lx = w[0] * m.b00 + w[1] * m.b10 + w[2] * m.b20;
+        ly = w[1] * m.b11 + w[2] * m.b21;
+        lz = w[2] * m.b22;
+    } else {
+        lx = x - g.low[0] - cc[0] / g.inv_edge[0];
+        ly = y - g.low[1] - cc[1] / g.inv_edge[1];
+        lz = z - g.low[2] - cc[2] / g.inv_edge[2];
+    }
+    a.slpos[s] = make_float4((float)lx, (float)ly, (float)lz, __int_as_float(i));
 }
 
 __global__ void k_identity_order(NlArgs a)
@@ -340,6 +367,8 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
     __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_queue[NL_WARPS][64];
+    __shared__ int s_run_start[NL_WARPS][32], s_run_pref[NL_WARPS][32];
+    __shared__ float s_run_shift[NL_WARPS][27][3];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int s = blockIdx.x * NL_WARPS + wib;
@@ -441,13 +470,105 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
                 }
             }
         };
-        GridDev g{};
-        int cell = 0;
         if (a.strategy == NNP_STRATEGY_CELL) {
-            g = *a.grid;
-            cell = a.cell_id[io];
+            // The 27 surrounding cells as ONE candidate stream: lane r < 27 looks up cell r's run in
+            // the sorted order and the displacement of its corner from the own cell's (the adjacent
+            // periodic image where the neighbourhood wraps, so no rounding to the minimum image is
+            // needed); every iteration then screens 32 consecutive candidates of the concatenated
+            // runs, whatever cell boundaries fall between them.
+            const GridDev g = *a.grid;
+            const int cell = a.cell_id[io];
+            const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
+            float cv[3][3];   // Cartesian step from one cell to the next along each grid axis
+            if (a.periodic) {
+                cv[0][0] = (float)(m.b00 / m0); cv[0][1] = 0.0f;                cv[0][2] = 0.0f;
+                cv[1][0] = (float)(m.b10 / m1); cv[1][1] = (float)(m.b11 / m1); cv[1][2] = 0.0f;
+                cv[2][0] = (float)(m.b20 / m2); cv[2][1] = (float)(m.b21 / m2); cv[2][2] = (float)(m.b22 / m2);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) cv[k][c] = k == c ? (float)(1.0 / g.inv_edge[k]) : 0.0f;
+            }
+            int r_start = 0, r_len = 0;
+            if (lane < 27) {
+                const int o0 = lane / 9 - 1, o1 = (lane / 3) % 3 - 1, o2 = lane % 3 - 1;
+                int n0 = cell / (m1 * m2) + o0, n1 = (cell / m2) % m1 + o1, n2 = cell % m2 + o2;
+                bool inside = true;
+                if (a.periodic) {
+                    n0 = n0 < 0 ? n0 + m0 : (n0 >= m0 ? n0 - m0 : n0);
+                    n1 = n1 < 0 ? n1 + m1 : (n1 >= m1 ? n1 - m1 : n1);
+                    n2 = n2 < 0 ? n2 + m2 : (n2 >= m2 ? n2 - m2 : n2);
+                } else {
+                    inside = n0 >= 0 && n0 < m0 && n1 >= 0 && n1 < m1 && n2 >= 0 && n2 < m2;
+                }
+                if (inside) {
+                    const int flat = (n0 * m1 + n1) * m2 + n2;
+                    r_start = a.cell_start[flat];
+                    r_len = a.cell_start[flat + 1] - r_start;
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    s_run_shift[wib][lane][c] = o0 * cv[0][c] + o1 * cv[1][c] + o2 * cv[2][c];
+            }
+            int incl = r_len;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int up = __shfl_up_sync(NNP_FULL_MASK, incl, d);
+                if (lane >= d) incl += up;
+            }
+            const int total = __shfl_sync(NNP_FULL_MASK, incl, 31);
+            s_run_start[wib][lane] = r_start;
+            s_run_pref[wib][lane] = lane < 27 ? incl - r_len : 0x7fffffff;   // exclusive; sentinel past the last run
+            __syncwarp();
+            // window widened by the screen's error: the local coordinates, the shift and their
+            // differences are each good to 2^-24 of the cell's extent
+            float ext = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ext += sqrtf(cv[k][0] * cv[k][0] + cv[k][1] * cv[k][1] + cv[k][2] * cv[k][2]);
+            const float slack = 4.0e-6f * ext;
+            const float r_hi = sqrtf((float)m.hi2) * 1.000001f + slack;
+            const float r_lo = sqrtf((float)m.lo2) * 0.999999f - slack;
+            const float hi2w = r_hi * r_hi * 1.000001f;
+            const float lo2w = r_lo > 0.0f ? r_lo * r_lo * 0.999999f : -1.0f;
+            const bool one_sample = a.n_samples == 1;
+            const float4 la = a.slpos[s];
+            const int *pref = s_run_pref[wib];
+            for (int base = 0; base < total; base += 32) {
+                const int idx = base + lane;
+                bool pass = false;
+                int t = 0;
+                if (idx < total) {
+                    int r = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (pref[r + step] <= idx) r += step;
+                    t = s_run_start[wib][r] + (idx - pref[r]);
+                    const float4 lb = a.slpos[t];
+                    const int jo = __float_as_int(lb.w);
+                    if ((one_sample || a.sbatch[t] == bi) && jo != io && (full || jo > io)) {
+                        const float fx = (la.x - lb.x) - s_run_shift[wib][r][0];
+                        const float fy = (la.y - lb.y) - s_run_shift[wib][r][1];
+                        const float fz = (la.z - lb.z) - s_run_shift[wib][r][2];
+                        const float d2 = fx * fx + fy * fy + fz * fz;
+                        pass = d2 <= hi2w && d2 >= lo2w;
+                    }
+                }
+                const unsigned mk = __ballot_sync(NNP_FULL_MASK, pass);
+                if (pass) queue[qn + __popc(mk & lt_mask)] = t;
+                qn += __popc(mk);
+                __syncwarp();
+                if (qn >= 32) {
+                    const int tq = queue[qn - 32 + lane];
+                    qn -= 32;
+                    exact_step(tq, true);
+                    __syncwarp();
+                }
+            }
+        } else {
+            GridDev g{};
+            visit_runs(a, g, 0, bi, process);
         }
-        visit_runs(a, g, cell, bi, process);
         if (qn > 0) {
             const bool valid = lane < qn;
             exact_step(valid ? queue[lane] : 0, valid);
@@ -577,6 +698,7 @@ size_t carve(NlArgs &a, const nnp_nl_params *p, void *ws)
     a.stage_w = stage_width(p);
     a.stage_t = ar.take<int>(n * (size_t)a.stage_w);
     a.spos = ar.take<double>(3 * n);
+    a.slpos = ar.take<float4>(n);
     a.bounds_partial = ar.take<double>(6 * BOUNDS_BLOCKS);
     a.grid = ar.take<GridDev>(1);
     return ar.bytes();
