@@ -209,6 +209,7 @@ class TensorNet:
         self.embed_projection = embed_projection
         self._plans: Dict[tuple, _Plan] = {}
         self._last_plan: Optional[_Plan] = None
+        self._z_key, self._z_proj = None, False
         self._capacity_hint: Dict[tuple, int] = {}
         self._upload()
 
@@ -309,6 +310,26 @@ class TensorNet:
             species = species.numpy()
         present = np.bincount(np.asarray(species).astype(np.int64, copy=False).ravel(), minlength=1)
         return int(np.count_nonzero(present)) <= self.PROJECTION_MAX_SPECIES
+
+    def _species_checked(self, z_t, n: int, check: bool, remember: bool = False) -> bool:
+        """Range check of the species codes (on whichever side they live: host tensors cost no
+        device reduction and no synchronisation) and the projection decision.  Both depend on the
+        codes only, so the answer is remembered for a tensor that has not been written since
+        (same storage and version counter), as in an MD loop; arrays that torch cannot track
+        (numpy inputs) are checked every time."""
+        key = (z_t.data_ptr(), z_t._version, n, str(z_t.device), check) if remember else None
+        if key is not None and key == self._z_key:
+            return self._z_proj
+        if check:
+            z_min, z_max = (int(v) for v in self._torch.aminmax(z_t))
+            if z_min < 0:
+                raise ValidationError(f"species codes must be >= 0, got {z_min}")
+            if z_max >= self.config.max_z:
+                raise ValidationError(
+                    f"species code {z_max} is out of range for max_z={self.config.max_z}")
+        proj = self._use_projection(z_t, n, count=check)
+        self._z_key, self._z_proj = key, proj
+        return proj
 
     def _plan(self, n: int, n_samples: int, box: Optional[Box], capacity: int, pos_is_f32: bool,
               proj: bool = False) -> _Plan:
@@ -420,26 +441,20 @@ class TensorNet:
                 n_samples = int(batch_t[-1]) + 1
         box_obj = self._as_box(box)
         capacity = self._capacity_hint.get((n, n_samples), self.neighbor_capacity(n))
-        proj = self._use_projection(z_t, n, count=check)
+        proj = self._species_checked(z_t, n, check, remember=isinstance(z, torch.Tensor))
         for _ in range(32):
             plan = self._plan(n, n_samples, box_obj, capacity, pos_t.dtype == torch.float32, proj)
             self._last_plan = plan
-            if check:
-                # species range check on whichever side the codes already live (host tensors: no
-                # device reduction and no extra synchronisation per call)
-                z_max = int(z_t.max())
-                if z_max >= self.config.max_z:
-                    raise ValidationError(
-                        f"species code {z_max} is out of range for max_z={self.config.max_z}")
-            plan.z.copy_(z_t.to(device=dev, dtype=torch.int32, non_blocking=True))
+            # straight into the plan's buffers: one host-to-device copy per input (a dtype change,
+            # if any, is made on the way), no intermediate device tensors
+            plan.z.copy_(z_t, non_blocking=True)
             if batch_t is not None:
-                plan.batch.copy_(batch_t.to(device=dev, dtype=torch.int32, non_blocking=True))
+                plan.batch.copy_(batch_t, non_blocking=True)
                 plan.batch_is_zero = False
             elif not plan.batch_is_zero:
                 plan.batch.zero_()
                 plan.batch_is_zero = True
-            (plan.pos32 if plan.pos32 is not None else plan.pos64).copy_(
-                pos_t.to(device=dev, non_blocking=True))
+            (plan.pos32 if plan.pos32 is not None else plan.pos64).copy_(pos_t, non_blocking=True)
             self._launch(plan)
             if not check:
                 break

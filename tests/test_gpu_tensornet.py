@@ -209,6 +209,22 @@ def test_evaluate_call_shapes_and_validation(rng):
         model.evaluate(system, other)
     with pytest.raises(P.ValidationError, match="out of range"):
         model.evaluate(P.build_system(pos, np.full(len(pos), 11), batch=batch))
+    # forward(): the species check is remembered for an unmodified tensor and redone after a write
+    zt, pt = torch.as_tensor(z.copy()), torch.as_tensor(pos, dtype=torch.float32)
+    e1, _ = model(zt, pt, torch.as_tensor(batch))
+    e2, _ = model(zt, pt, torch.as_tensor(batch))
+    assert torch.equal(e1, e2)
+    zt[0] = 10
+    with pytest.raises(P.ValidationError, match="out of range"):
+        model(zt, pt, torch.as_tensor(batch))
+    zt[0] = -1
+    with pytest.raises(P.ValidationError, match=">= 0"):
+        model(zt, pt, torch.as_tensor(batch))
+    zn = z.copy()
+    model(zn, pos.astype(np.float32), batch)
+    zn[0] = 12                                          # numpy input mutated in place: checked every call
+    with pytest.raises(P.ValidationError, match="out of range"):
+        model(zn, pos.astype(np.float32), batch)
 
 
 def test_invariances_on_device(rng):
