@@ -31,6 +31,10 @@ struct GridDev {
     int ncell;
     double low[3];
     double inv_edge[3];
+    // the row scan's single-precision screen: Cartesian step between adjacent cells along each grid
+    // axis, and the squared-distance window widened by the screen's error bound
+    float cv[3][3];
+    float hi2w, lo2w;
 };
 
 struct Metric {
@@ -188,6 +192,28 @@ __global__ void k_grid_setup(NlArgs a, int n_partial)
         for (int k = 0; k < 3; ++k) g.inv_edge[k] = (double)g.dims[k] / extent[k];
     }
     g.ncell = g.dims[0] * g.dims[1] * g.dims[2];
+    {
+        const Metric &m = a.metric;
+        double cv[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (a.periodic) {
+            cv[0][0] = m.b00 / g.dims[0];
+            cv[1][0] = m.b10 / g.dims[1]; cv[1][1] = m.b11 / g.dims[1];
+            cv[2][0] = m.b20 / g.dims[2]; cv[2][1] = m.b21 / g.dims[2]; cv[2][2] = m.b22 / g.dims[2];
+        } else {
+            for (int k = 0; k < 3; ++k) cv[k][k] = 1.0 / g.inv_edge[k];
+        }
+        double ext = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            ext += sqrt(cv[k][0] * cv[k][0] + cv[k][1] * cv[k][1] + cv[k][2] * cv[k][2]);
+            for (int c = 0; c < 3; ++c) g.cv[k][c] = (float)cv[k][c];
+        }
+        // local coordinates, shift and their differences are each good to 2^-24 of the cell's
+        // extent: 8 roundings per component, x sqrt(3), x 5 margin
+        const double slack = 4.0e-6 * ext;
+        const double r_hi = sqrt(m.hi2) * 1.000001 + slack, r_lo = sqrt(m.lo2) * 0.999999 - slack;
+        g.hi2w = (float)(r_hi * r_hi * 1.000002);
+        g.lo2w = r_lo > 0.0 ? (float)(r_lo * r_lo * 0.999998) : -1.0f;
+    }
     *a.grid = g;
     a.counts[2] = g.ncell;
 }
@@ -479,17 +505,6 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
             const GridDev g = *a.grid;
             const int cell = a.cell_id[io];
             const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
-            float cv[3][3];   // Cartesian step from one cell to the next along each grid axis
-            if (a.periodic) {
-                cv[0][0] = (float)(m.b00 / m0); cv[0][1] = 0.0f;                cv[0][2] = 0.0f;
-                cv[1][0] = (float)(m.b10 / m1); cv[1][1] = (float)(m.b11 / m1); cv[1][2] = 0.0f;
-                cv[2][0] = (float)(m.b20 / m2); cv[2][1] = (float)(m.b21 / m2); cv[2][2] = (float)(m.b22 / m2);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) cv[k][c] = k == c ? (float)(1.0 / g.inv_edge[k]) : 0.0f;
-            }
             int r_start = 0, r_len = 0;
             if (lane < 27) {
                 const int o0 = lane / 9 - 1, o1 = (lane / 3) % 3 - 1, o2 = lane % 3 - 1;
@@ -509,7 +524,7 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
                 }
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    s_run_shift[wib][lane][c] = o0 * cv[0][c] + o1 * cv[1][c] + o2 * cv[2][c];
+                    s_run_shift[wib][lane][c] = o0 * g.cv[0][c] + o1 * g.cv[1][c] + o2 * g.cv[2][c];
             }
             int incl = r_len;
 #pragma unroll
@@ -521,16 +536,7 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
             s_run_start[wib][lane] = r_start;
             s_run_pref[wib][lane] = lane < 27 ? incl - r_len : 0x7fffffff;   // exclusive; sentinel past the last run
             __syncwarp();
-            // window widened by the screen's error: the local coordinates, the shift and their
-            // differences are each good to 2^-24 of the cell's extent
-            float ext = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) ext += sqrtf(cv[k][0] * cv[k][0] + cv[k][1] * cv[k][1] + cv[k][2] * cv[k][2]);
-            const float slack = 4.0e-6f * ext;
-            const float r_hi = sqrtf((float)m.hi2) * 1.000001f + slack;
-            const float r_lo = sqrtf((float)m.lo2) * 0.999999f - slack;
-            const float hi2w = r_hi * r_hi * 1.000001f;
-            const float lo2w = r_lo > 0.0f ? r_lo * r_lo * 0.999999f : -1.0f;
+            const float hi2w = g.hi2w, lo2w = g.lo2w;     // window widened by the screen's error bound
             const bool one_sample = a.n_samples == 1;
             const float4 la = a.slpos[s];
             const int *pref = s_run_pref[wib];
