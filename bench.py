@@ -231,9 +231,21 @@ def neighbor_sweep(torch, peak_gbs):
             stop.record()
             torch.cuda.synchronize()
             us = 1000.0 * start.elapsed_time(stop) / reps
+            # the reference times deterministic=False (bench.py:133-138): same list, rows not ranked
+            eng_u = NeighborEngine(n, 1, cap, box, 0.0, CUTOFF, code, dims, max_cells, _lib.NL_UNSORTED)
+            eng_u.build(dev_pos, dev_batch)
+            torch.cuda.synchronize()
+            start.record()
+            for _ in range(reps):
+                eng_u.build(dev_pos, dev_batch)
+            stop.record()
+            torch.cuda.synchronize()
+            us_unsorted = 1000.0 * start.elapsed_time(stop) / reps
+            del eng_u
             ncell = int(eng.counts[2].item()) if strategy == "cell" else 0
             nbytes = 48 * n + 8 * ncell + 40 * pairs      # float64 outputs: 8 + 24 + 8 B per row
-            rows.append({"n": n, "strategy": strategy, "us_per_call": round(us, 2), "pairs": pairs,
+            rows.append({"n": n, "strategy": strategy, "us_per_call": round(us, 2),
+                         "us_per_call_unsorted": round(us_unsorted, 2), "pairs": pairs,
                          "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peak_gbs, 4)})
             del eng
         del dev_pos, dev_batch

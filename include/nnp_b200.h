@@ -50,6 +50,8 @@ typedef void *nnp_stream_t; /* a cudaStream_t */
 #define NNP_NL_RENUMBER 4   /* rows/cols in cell-sorted atom numbering (internal model path) */
 #define NNP_NL_F32_OUT 8    /* deltas/distances written as float32 instead of float64 */
 #define NNP_NL_NO_PAD 16    /* do not write -1/0 sentinels into the unused tail */
+#define NNP_NL_UNSORTED 32  /* NeighborSpec.deterministic = False (neighbors.py:44,221): rows stay grouped by
+                               receiver (row_ptr is valid) but the order inside a row is unspecified */
 
 const char *nnp_last_error(void);
 int nnp_version(void);

@@ -20,7 +20,7 @@ NNP_ERR_CUDA = -3
 
 BOX_KIND = {"none": 0, "orthorhombic": 1, "triclinic": 2}
 STRATEGY_BRUTE, STRATEGY_CELL = 0, 1
-NL_FULL_LIST, NL_SELF_LOOPS, NL_RENUMBER, NL_F32_OUT, NL_NO_PAD = 1, 2, 4, 8, 16
+NL_FULL_LIST, NL_SELF_LOOPS, NL_RENUMBER, NL_F32_OUT, NL_NO_PAD, NL_UNSORTED = 1, 2, 4, 8, 16, 32
 TN_MAX_LAYERS = 8
 
 EXPORTED_SYMBOLS = (

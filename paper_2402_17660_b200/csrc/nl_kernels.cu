@@ -606,8 +606,11 @@ __global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
     for (int e = lane; e < cnt; e += 32) {
         const int col = ((volatile int *)list_col)[e];
         const int t = ((volatile int *)list_t)[e];
-        int rank = 0;
-        for (int q = 0; q < cnt; ++q) rank += (((volatile int *)list_col)[q] < col);
+        int rank = e;                                   // NNP_NL_UNSORTED: the order of discovery
+        if (!(a.flags & NNP_NL_UNSORTED)) {
+            rank = 0;
+            for (int q = 0; q < cnt; ++q) rank += (((volatile int *)list_col)[q] < col);
+        }
         const size_t idx = (size_t)row_start + rank;
         a.pairs[2 * idx] = row;
         a.pairs[2 * idx + 1] = col;

@@ -203,8 +203,10 @@ class NeighborEngine:
 def build_neighbor_list(system: System, spec: NeighborSpec) -> NeighborList:
     """Enumerate all in-batch pairs inside the distance window on the GPU.
 
-    Drop-in for ``nnpkit.build_neighbor_list`` (neighbors.py:136-235).  ``deterministic=False``
-    is accepted and still returns the (i, j)-sorted order (any order is valid then).
+    Drop-in for ``nnpkit.build_neighbor_list`` (neighbors.py:136-235).  With
+    ``deterministic=False`` rows are still grouped by ``i`` but the order inside a group is the
+    order of discovery (the reference promises no order then, neighbors.py:221); the in-row
+    ranking pass is skipped.
     """
     torch = _lib.require_cuda()
     n = system.n_atoms
@@ -212,7 +214,8 @@ def build_neighbor_list(system: System, spec: NeighborSpec) -> NeighborList:
     check_cutoff_against_box(box, spec.cutoff_upper)
     code, dims, max_cells, notes = plan_strategy(n, box, spec.cutoff_upper, spec.strategy)
     flags = (_lib.NL_FULL_LIST if spec.full_list else 0) | (
-        _lib.NL_SELF_LOOPS if spec.include_self_loops else 0)
+        _lib.NL_SELF_LOOPS if spec.include_self_loops else 0) | (
+        0 if spec.deterministic else _lib.NL_UNSORTED)
     eng = NeighborEngine(n, system.n_samples, spec.capacity, box, spec.cutoff_lower,
                          spec.cutoff_upper, code, dims, max_cells, flags)
     pos = torch.from_numpy(np.array(system.positions, dtype=np.float64, order="C")).to(eng.device)

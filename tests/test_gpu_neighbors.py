@@ -233,3 +233,27 @@ def test_full_size_sweep_point_properties():
     assert rp[0] == 0 and rp[-1] == full.count and np.all(np.diff(rp) >= 0)
     fp = full.pairs[: full.count].cpu().numpy()
     assert np.array_equal(fp[:, 0], np.repeat(np.arange(n), np.diff(rp)))
+
+
+def test_nondeterministic_lists_hold_the_same_rows_grouped_by_receiver(rng):
+    """deterministic=False (the reference's timing mode, neighbors.py:44,221) skips the in-row
+    ranking: the same rows, bit for bit, grouped by i, in an unspecified order inside a group."""
+    _, box = random_reduced_box(rng, 13.0, 17.0, kind="triclinic")
+    pos = rng.uniform(0, 1, (400, 3)) @ box
+    batch = random_batch(rng, 400, 3)
+    for strategy in ("cell", "brute"):
+        for full, loops in ((False, False), (True, True)):
+            system = make_system(pos, batch, box)
+            kw = dict(cutoff_upper=4.0, capacity=40000, strategy=strategy, full_list=full,
+                      include_self_loops=loops)
+            sorted_nl = P.build_neighbor_list(system, P.NeighborSpec(**kw)).as_reference()
+            loose = P.build_neighbor_list(system, P.NeighborSpec(deterministic=False, **kw))
+            host = loose.as_reference()
+            c = sorted_nl.count
+            assert loose.count == c
+            assert np.all(np.diff(host.pairs[:c, 0]) >= 0)                     # still CSR by receiver
+            order = np.lexsort((host.pairs[:c, 1], host.pairs[:c, 0]))
+            assert np.array_equal(host.pairs[:c][order], sorted_nl.pairs[:c])
+            assert np.array_equal(host.deltas[:c][order], sorted_nl.deltas[:c])
+            assert np.array_equal(host.distances[:c][order], sorted_nl.distances[:c])
+            assert np.all(host.pairs[c:] == -1)
