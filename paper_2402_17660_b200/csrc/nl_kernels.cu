@@ -388,7 +388,7 @@ __device__ __forceinline__ bool prefilter(const NlArgs &a, double ax, double ay,
 }
 
 template <bool FILL, typename OutT>
-__global__ void __launch_bounds__(NL_THREADS) k_rows(NlArgs a)
+__global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
 {
     __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
