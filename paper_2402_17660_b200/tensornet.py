@@ -287,7 +287,7 @@ class TensorNet:
         # small samples: all-pairs inside each sample; otherwise the cell list
         return "brute" if n / max(n_samples, 1) < 1024 else "cell"
 
-    PROJECTION_MIN_ATOMS = 4096   # below this the two extra GEMM launches cost more than they save
+    PROJECTION_MIN_ATOMS = 1024   # measured (tools/proj_threshold.py): even at 1 000 atoms, 6 % faster at 2 489; slower at 22
     PROJECTION_MAX_SPECIES = 4
 
     def _use_projection(self, species, n: int, count: bool = True) -> bool:
