@@ -718,7 +718,8 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
     // a GEMM over N_atoms rows costs up to ~8k atoms; the mma.sync tile is quicker there
     // (measured at 2 489 atoms: 0.15 vs 0.24 ms for the eight dense GEMMs)
     const bool streamable = maxN == 128 && b.g[0].K == 128;
-    const bool tiny = g_nnp_gemm_use_mma == 5 && (maxM <= 1024 || (!streamable && maxM <= 8192));
+    static const int dense_tiny_m = getenv("NNP_DENSE_TINY_M") ? atoi(getenv("NNP_DENSE_TINY_M")) : 8192;
+    const bool tiny = g_nnp_gemm_use_mma == 5 && (maxM <= 1024 || (!streamable && maxM <= dense_tiny_m));
     if (g_nnp_gemm_use_mma >= 2 && !tiny) {
         int rc = -100;
         if (g_nnp_gemm_use_mma == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);
