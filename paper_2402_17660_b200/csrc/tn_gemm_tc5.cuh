@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
             mbar_init(&tfull_bar[a], 1);
             mbar_init(&tempty_bar[a], ST_EPI_WARPS);        // one arrival per epilogue warp
         }
-        mbar_init(&w_bar, 128);
+        mbar_init(&w_bar, 32 * ST_EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -412,13 +412,18 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = tmem_base_s;
 
-    // weights -> tensor memory (once): lane = output channel n, column k (hi) / 128 + k (lo)
-    if (warp < 4) {
-        const int n = warp * 32 + lane;
+    // weights -> tensor memory (once): lane = output channel n, column k (hi) / 128 + k (lo).
+    // All eight epilogue warps take part (two per TMEM lane quadrant, half of K each, two 16-column
+    // blocks in flight): the staging is a chain of dependent L2 round trips, ~15 us of fixed cost per
+    // launch when four warps walked all of K one block at a time.
+    if (warp < 4 || warp >= 13) {
+        const int quad_w = warp & 3;
+        const int n = quad_w * 32 + lane;
         const float *wrow = g.W + (size_t)n * K;
-        const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int k0 = 0; k0 < K; k0 += 16) {
+        const uint32_t lane_addr = tmem_base + ((uint32_t)(quad_w * 32) << 16);
+        const int kbeg = warp < 4 ? 0 : K / 2;
+#pragma unroll 2
+        for (int k0 = kbeg; k0 < kbeg + K / 2; k0 += 16) {
             uint32_t hi[16], lo[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
