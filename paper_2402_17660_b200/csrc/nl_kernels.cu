@@ -640,15 +640,18 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
 template <typename OutT>
 __global__ void k_pad_tail(NlArgs a)
 {
+    // fixed grid, element-wise over the three tails (the row count is only known on the device, so a
+    // grid sized for the whole capacity would launch mostly idle blocks)
     const int total = a.row_ptr[a.n];
-    const int64_t idx = (int64_t)total + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (total > a.capacity || idx >= a.capacity) return;
-    a.pairs[2 * idx] = -1;
-    a.pairs[2 * idx + 1] = -1;
-    OutT *deltas = static_cast<OutT *>(a.deltas);
-    OutT *dists = static_cast<OutT *>(a.dists);
-    deltas[3 * idx] = deltas[3 * idx + 1] = deltas[3 * idx + 2] = (OutT)0;
-    dists[idx] = (OutT)0;
+    if (total > a.capacity) return;
+    const int64_t rows = (int64_t)a.capacity - total;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    int *pairs = a.pairs + 2 * (int64_t)total;
+    OutT *deltas = static_cast<OutT *>(a.deltas) + 3 * (int64_t)total;
+    OutT *dists = static_cast<OutT *>(a.dists) + total;
+    for (int64_t i = tid; i < 2 * rows; i += stride) pairs[i] = -1;
+    for (int64_t i = tid; i < 3 * rows; i += stride) deltas[i] = (OutT)0;
+    for (int64_t i = tid; i < rows; i += stride) dists[i] = (OutT)0;
 }
 
 __global__ void k_f32_to_f64(const float *__restrict__ src, double *__restrict__ dst, int64_t n)
@@ -858,9 +861,9 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
         { NNP_PROF("k_rows_fill", stream); k_rows<true, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
     if (!(p->flags & NNP_NL_NO_PAD)) {
         if (f32)
-            { NNP_PROF("k_pad_tail", stream); k_pad_tail<float><<<NNP_GRID(nnp_blocks(a.capacity, 256)), 256, 0, stream>>>(a); }
+            { NNP_PROF("k_pad_tail", stream); k_pad_tail<float><<<NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream>>>(a); }
         else
-            { NNP_PROF("k_pad_tail", stream); k_pad_tail<double><<<NNP_GRID(nnp_blocks(a.capacity, 256)), 256, 0, stream>>>(a); }
+            { NNP_PROF("k_pad_tail", stream); k_pad_tail<double><<<NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream>>>(a); }
     }
     NNP_CHECK_LAUNCH("neighbor rows");
     return NNP_OK;
