@@ -111,6 +111,7 @@ __global__ void k_sample_ptr(const int *__restrict__ batch, int n, int n_samples
     if (b < 4) counts[b] = 0;
     if (b > n_samples) return;
     int lo = 0, hi = n;
+    if (n_samples == 1) lo = hi = (b == 0 ? 0 : n);      // one sample: no search (15 dependent loads)
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (batch[mid] < b) lo = mid + 1; else hi = mid;
