@@ -3,13 +3,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload C|A|D|E] [--no-sweep] [--no-cpu]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N ... bench.py --gpus N ...
+    (``--gpus N`` without RANK in the environment re-launches itself that way)
 
 A "step" is one pass of the hot path over one batch of synthetic input: cutoff neighbor
 search (cell list) + TensorNet forward + analytic force sweep, replayed as one CUDA graph.
 Default workload = BASELINE.json configs[2]: 2-layer, 128-channel TensorNet on the synthetic
 23,558-atom periodic box (the configuration the north-star target is quoted on).  With
-N > 1 the box does not shard ("replicas only"), so every rank steps its own
-replica ("weak" scaling); `--workload D` shards 8192 molecules by whole molecules instead.
+N > 1 the default workload becomes D (BASELINE.json configs[3]): the batch of 8192 molecules is
+sharded by whole molecules over the ranks ("strong" scaling, no collective inside the step) and
+the final all_gather of energies and forces is INSIDE the timed region.  A single periodic box
+does not shard ("replicas only"): `--workload C|E` with N > 1 steps N replicas.
+Layer counts follow BASELINE.json: 2 layers for A, C, D and 3 layers for E.
 
 One JSON line on stdout (rank 0).  `value` = whole-job steps/s with inputs resident in HBM;
 `e2e` = the same through TensorNet.forward with pinned HOST buffers (H2D of species+positions
@@ -33,7 +38,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TensorNet energy+forces steps/s (neighbor search included)"
-CHANNELS, LAYERS, NUM_RBF, CUTOFF = 128, 2, 32, 5.0
+CHANNELS, NUM_RBF, CUTOFF = 128, 32, 5.0
+LAYERS_OF = {"A": 2, "C": 2, "D": 2, "E": 3}       # BASELINE.json configs
 
 
 def load_peaks():
@@ -116,10 +122,10 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def algorithmic_bytes(n_atoms: int, n_edges: int, n_cells: int):
+def algorithmic_bytes(n_atoms: int, n_edges: int, n_cells: int, layers: int):
     """Compulsory HBM bytes; gathers counted once per pass."""
     T = 9 * CHANNELS * 4
-    L = LAYERS
+    L = layers
     per_kernel = {
         "k_edge_message": 4 * T * n_atoms + 20 * n_edges,      # read Y' (gather + own), write M and Q
         "k_edge_message_bwd": 4 * T * n_atoms + 28 * n_edges,  # read G_M, Y', G_Y; write G_Y; edges
@@ -152,9 +158,9 @@ def cpu_oracle_step(sample_atoms: int, full_nl: bool = True, seed: int = 11):
         t_nl = time.perf_counter() - t0
     edge = (sample_atoms / 0.09776) ** (1.0 / 3.0)
     z, pos, batch, box = synth.config_c_box(n=sample_atoms, edge=edge, seed=seed)
-    cfg = TNConfig(embedding_dimension=CHANNELS, num_layers=LAYERS, num_rbf=NUM_RBF, cutoff_upper=CUTOFF)
+    cfg = TNConfig(embedding_dimension=CHANNELS, num_layers=LAYERS_OF["C"], num_rbf=NUM_RBF, cutoff_upper=CUTOFF)
     params = init_params(cfg, 0)
-    ocfg = T.OracleConfig(CHANNELS, LAYERS, NUM_RBF, 0.0, CUTOFF)
+    ocfg = T.OracleConfig(CHANNELS, LAYERS_OF["C"], NUM_RBF, 0.0, CUTOFF)
     t0 = time.perf_counter()
     nl = O.build_neighbor_list(pos, batch, box, CUTOFF, 2 * 64 * sample_atoms, full_list=True,
                                include_self_loops=True)
@@ -191,8 +197,10 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "C: 23,558-atom periodic cubic box (62.23 A), water-like species",
-                   "channels": CHANNELS, "layers": LAYERS, "num_rbf": NUM_RBF, "cutoff": CUTOFF},
+        "config": {"workload": (f"C-sample: neighbor list on the full 23,558-atom box + TensorNet on a {sample}-atom "
+                                f"periodic box of config C's density, TensorNet time scaled by 23558/{sample}"),
+                   "sampled_atoms": sample, "full_atoms": 23558, "extrapolated": True, "same_config": False,
+                   "channels": CHANNELS, "layers": LAYERS_OF["C"], "num_rbf": NUM_RBF, "cutoff": CUTOFF},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -200,9 +208,12 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def neighbor_sweep(torch, peak_gbs):
-    """Config B: neighbor-list us/call over particle counts (half list, like bench.py:133-138)."""
+def neighbor_sweep(torch, peak_gbs, with_cpu=True):
+    """Config B: neighbor-list us/call over particle counts (half list, like bench.py:133-138 of
+    the reference), with the C oracle (the CPU port of the reference's numba kernels, one core,
+    one call) timed beside every point it finishes in seconds."""
     import paper_2402_17660_b200 as P
+    from oracle import neighbors_oracle as O
     from paper_2402_17660_b200 import _lib, synth
     from paper_2402_17660_b200.neighbors import NeighborEngine, plan_strategy
 
@@ -244,9 +255,17 @@ def neighbor_sweep(torch, peak_gbs):
             del eng_u
             ncell = int(eng.counts[2].item()) if strategy == "cell" else 0
             nbytes = 48 * n + 8 * ncell + 40 * pairs      # float64 outputs: 8 + 24 + 8 B per row
-            rows.append({"n": n, "strategy": strategy, "us_per_call": round(us, 2),
-                         "us_per_call_unsorted": round(us_unsorted, 2), "pairs": pairs,
-                         "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peak_gbs, 4)})
+            row = {"n": n, "strategy": strategy, "us_per_call": round(us, 2),
+                   "us_per_call_unsorted": round(us_unsorted, 2), "pairs": pairs,
+                   "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peak_gbs, 4)}
+            if with_cpu and (n <= 262144 if strategy == "cell" else n <= 16384):
+                t0 = time.perf_counter()
+                # deterministic=False like the reference's own sweep: compare with us_per_call_unsorted
+                ref = O.build_neighbor_list(pos, batch, boxm, CUTOFF, cap, strategy=strategy, deterministic=False)
+                row["cpu_us_per_call"] = round(1e6 * (time.perf_counter() - t0), 1)
+                row["cpu_cores"] = 1
+                row["cpu_pairs_equal"] = bool(ref.count == pairs)
+            rows.append(row)
             del eng
         del dev_pos, dev_batch
         torch.cuda.empty_cache()
@@ -259,7 +278,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C", choices=["A", "C", "D", "E"])
+    ap.add_argument("--workload", default=None, choices=["A", "C", "D", "E"],
+                    help="default: C on one GPU, D (sharded by molecule) on several")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-md", action="store_true")
@@ -268,6 +288,16 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "RANK" not in os.environ:
+        # one process per GPU: re-launch under torchrun exactly as the driver does
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
 
     import torch
     import torch.distributed as dist
@@ -275,6 +305,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        args.workload = "C" if world == 1 else "D"
+    LAYERS = LAYERS_OF[args.workload]
+    sharded = world > 1 and args.workload == "D"
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
     torch.cuda.set_device(local)
@@ -286,6 +320,11 @@ def main():
     from paper_2402_17660_b200 import _lib
 
     peak_gbs, peak_src = load_peaks()
+    full_batch = None
+    if sharded:
+        from paper_2402_17660_b200 import synth
+
+        full_batch = synth.config_d_molecules(8192)[2]
     z, pos, batch, box, desc = workload(args.workload, rank, world)
     n_atoms = len(pos)
     n_samples = int(batch[-1]) + 1
@@ -323,17 +362,30 @@ def main():
             a[1] = cnt
     kernel_ms = {k: round(v[0], 5) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
-    # ---- device-resident timing: K graph replays, CUDA events, max over ranks
+    # ---- device-resident timing: K graph replays, CUDA events, max over ranks.  Sharded batch
+    # (workload D on several GPUs): every step ends with the all_gather that returns all energies
+    # and forces to every rank (sharding.py), inside the timed region.
+    gather = None
+    if sharded:
+        from paper_2402_17660_b200.sharding import ResidentGather
+
+        gather = ResidentGather(full_batch, world, rank, torch.device("cuda", local))
+
+    def resident_step():
+        model.replay(plan)
+        if gather is not None:
+            gather(plan.energy, plan.forces)
+
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
     for _ in range(args.warmup):
-        model.replay(plan)
+        resident_step()
     barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for _ in range(args.steps):
-        model.replay(plan)
+        resident_step()
     stop.record()
     barrier()
     elapsed_ms = start.elapsed_time(stop)
@@ -348,11 +400,15 @@ def main():
     # ---- end to end through the public API with pinned host buffers
     z_h, pos_h = z_t.pin_memory(), pos_t.pin_memory()
     b_h = None if batch_t is None else batch_t.pin_memory()
-    e_h = torch.empty(n_samples, dtype=torch.float32).pin_memory()
-    f_h = torch.empty((n_atoms, 3), dtype=torch.float32).pin_memory()
+    out_samples = n_samples if gather is None else gather.n_samples
+    out_atoms = n_atoms if gather is None else gather.n_atoms
+    e_h = torch.empty(out_samples, dtype=torch.float32).pin_memory()
+    f_h = torch.empty((out_atoms, 3), dtype=torch.float32).pin_memory()
 
     def e2e_step():
         e, f = model.forward(z_h, pos_h, b_h, box, n_samples=n_samples, check=True, clone=False)
+        if gather is not None:
+            e, f = gather(e, f)
         e_h.copy_(e, non_blocking=True)
         f_h.copy_(f, non_blocking=True)
         torch.cuda.synchronize()
@@ -388,7 +444,7 @@ def main():
         return
 
     # ---- roofline of the dominant kernel and of the whole step
-    per_kernel_bytes, step_bytes, nl_bytes = algorithmic_bytes(n_atoms, n_edges, n_cells)
+    per_kernel_bytes, step_bytes, nl_bytes = algorithmic_bytes(n_atoms, n_edges, n_cells, LAYERS)
     dominant = next(iter(kernel_ms))
     launches = prof[dominant][1]
     roof = {"bound": "hbm", "kernel": dominant, "peak": peak_gbs, "unit": "GB/s", "peak_source": peak_src,
@@ -431,7 +487,10 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "atoms": n_atoms, "samples": n_samples, "directed_edges": n_edges,
                    "channels": CHANNELS, "layers": LAYERS, "num_rbf": NUM_RBF, "cutoff": CUTOFF,
-                   "parallelism": "replicas only" if args.workload != "D" else f"molecules/{world}",
+                   "parallelism": "replicas only" if args.workload != "D" else
+                                  f"whole molecules over {world} rank(s); all_gather of energies+forces inside the timed step"
+                                  if world > 1 else "one GPU",
+                   "atoms_are": "rank 0's shard" if sharded else "whole system",
                    "l2_note": "working set per step (saved activations ~1.3 GB) exceeds the 126 MB L2; no flush",
                    "msteps_per_day": round(86.4 / ms_per_step, 3)},
         "clocks": clocks,
@@ -474,7 +533,7 @@ def main():
                       "what": "neighbor search + TensorNet energy/forces + Langevin-middle integrator "
                               "(device Philox noise), one CUDA graph per step, float64 state"}
     if world == 1 and not args.no_sweep:
-        line["neighbor_sweep"] = neighbor_sweep(torch, peak_gbs)
+        line["neighbor_sweep"] = neighbor_sweep(torch, peak_gbs, with_cpu=not args.no_cpu)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

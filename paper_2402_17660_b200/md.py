@@ -232,11 +232,29 @@ class DeviceIntegrator:
             raise CapacityError(required=required, capacity=self.plan.capacity)
 
 
+def network_of(potential):
+    """The TensorNet a device MD loop integrates.  The reference integrates whatever
+    ``evaluate_auto`` returns for the composed potential (md.py:107-111, 192-204); the device loop
+    runs the network's captured step only, so a potential whose priors or ``derivative=False``
+    would change the forces is refused instead of being integrated wrongly."""
+    if not hasattr(potential, "network"):
+        return potential
+    if potential.network is None:
+        raise ValidationError("device MD needs a TensorNet network; a prior-only potential has none")
+    if len(potential.priors):
+        raise ValidationError(
+            "device MD integrates the network's forces only: a ComposedPotential with analytic "
+            "priors is not supported (evaluate it with evaluate_auto instead)")
+    if not potential.derivative:
+        raise ValidationError("device MD needs forces: potential.derivative is False")
+    return potential.network
+
+
 def langevin_middle_step(state: MDState, potential, dt_fs: float, temperature: float,
                          gamma_per_ps: float, max_num_neighbors: int = 64) -> MDState:
     """Advance one step; returns a new state sharing the RNG stream (md.py:114-145).
-    ``potential`` is a ``TensorNet`` (or a ``ComposedPotential`` wrapping one)."""
-    model = getattr(potential, "network", potential)
+    ``potential`` is a ``TensorNet`` (or a ``ComposedPotential`` wrapping one, without priors)."""
+    model = network_of(potential)
     integ = DeviceIntegrator(model, state.system, state.velocities, state.masses, temperature, state.seed)
     _, c2 = ou_coefficients(dt_fs, gamma_per_ps)
     noise = state.rng.standard_normal((state.masses.size, 3)) if c2 > 0.0 else None
@@ -273,7 +291,7 @@ def run_simulation(state: MDState, potential, steps: int, dt_fs: float, temperat
     (md.py:166-223).  Frame zero is the initial configuration; 1 + floor(steps/stride) frames."""
     if steps < 0 or stride < 1:
         raise ValidationError("steps must be >= 0 and stride >= 1")
-    model = getattr(potential, "network", potential)
+    model = network_of(potential)
     torch = _lib.require_cuda()
     trajectory = Trajectory(stride=stride, dt_fs=dt_fs, temperature_k=temperature,
                             gamma_per_ps=gamma_per_ps, seed=state.seed, species=state.system.species)

@@ -84,3 +84,45 @@ def evaluate_sharded(step: Callable, species, positions, batch, box=None, group=
         energy[rs0:rs1] = e_all[r][: rs1 - rs0]
         forces[ra0:ra1] = f_all[r][: ra1 - ra0]
     return energy, forces
+
+
+class ResidentGather:
+    """The gather at the end of a sharded step with every buffer allocated once: ``__call__`` takes
+    this rank's energies/forces (device tensors) and returns the full ``(energy[n_samples],
+    forces[N, 3])`` on every rank.  Two ``all_gather_into_tensor`` calls on padded per-rank slots
+    (ranks hold different atom counts), then the slots are packed; no host synchronisation, so a
+    benchmark can time K steps back to back with the collective inside the timed region."""
+
+    def __init__(self, batch, world_size: int, rank: int, device, group=None):
+        import torch
+
+        self.torch, self.group, self.world, self.rank = torch, group, world_size, rank
+        batch = np.asarray(batch)
+        self.shards = shard_by_molecule(batch, world_size)
+        self.n_samples, self.n_atoms = int(batch[-1]) + 1, len(batch)
+        self.max_s = max(s[3] - s[2] for s in self.shards)
+        self.max_a = max(s[1] - s[0] for s in self.shards)
+        f32 = dict(dtype=torch.float32, device=device)
+        self.e_pad = torch.zeros(self.max_s, **f32)
+        self.f_pad = torch.zeros((self.max_a, 3), **f32)
+        self.e_all = torch.empty(world_size * self.max_s, **f32)
+        self.f_all = torch.empty((world_size * self.max_a, 3), **f32)
+        self.energy = torch.empty(self.n_samples, **f32)
+        self.forces = torch.empty((self.n_atoms, 3), **f32)
+
+    def __call__(self, e_local, f_local):
+        import torch.distributed as dist
+
+        a0, a1, s0, s1 = self.shards[self.rank]
+        self.e_pad[: s1 - s0].copy_(e_local, non_blocking=True)
+        self.f_pad[: a1 - a0].copy_(f_local, non_blocking=True)
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.e_all, self.e_pad, group=self.group)
+            dist.all_gather_into_tensor(self.f_all, self.f_pad, group=self.group)
+        else:
+            self.e_all.copy_(self.e_pad)
+            self.f_all.copy_(self.f_pad)
+        for r, (ra0, ra1, rs0, rs1) in enumerate(self.shards):
+            self.energy[rs0:rs1] = self.e_all[r * self.max_s: r * self.max_s + rs1 - rs0]
+            self.forces[ra0:ra1] = self.f_all[r * self.max_a: r * self.max_a + ra1 - ra0]
+        return self.energy, self.forces

@@ -210,6 +210,7 @@ class TensorNet:
         self._plans: Dict[tuple, _Plan] = {}
         self._last_plan: Optional[_Plan] = None
         self._z_key, self._z_proj = None, False
+        self._b_key = None
         self._capacity_hint: Dict[tuple, int] = {}
         self._upload()
 
@@ -331,6 +332,25 @@ class TensorNet:
         self._z_key, self._z_proj = key, proj
         return proj
 
+    def _batch_checked(self, batch_t, n: int, n_samples: int, remember: bool = False) -> None:
+        """Sample codes must start at 0, never decrease, and stay below ``n_samples`` (what
+        ``build_system`` enforces in the reference, system.py): ``k_prep_nodes`` writes
+        ``sample_ptr[code]`` and the per-sample search bisects the codes.  Empty samples (gaps in
+        the codes) are allowed, as ``segment_sum`` allows them.  Remembered per unmodified tensor."""
+        key = (batch_t.data_ptr(), batch_t._version, n, n_samples, str(batch_t.device)) if remember else None
+        if key is not None and key == self._b_key:
+            return
+        torch = self._torch
+        if batch_t.dtype.is_floating_point or batch_t.dtype == torch.bool:
+            raise ValidationError("batch codes must be integers")
+        first, last = int(batch_t[0]), int(batch_t[-1])
+        if first < 0 or last >= n_samples:
+            raise ValidationError(
+                f"batch codes must lie in [0, n_samples): got first {first}, last {last}, n_samples {n_samples}")
+        if n > 1 and bool((batch_t[1:] < batch_t[:-1]).any()):
+            raise ValidationError("batch codes must be non-decreasing (atoms of one sample contiguous)")
+        self._b_key = key
+
     def _plan(self, n: int, n_samples: int, box: Optional[Box], capacity: int, pos_is_f32: bool,
               proj: bool = False) -> _Plan:
         torch, cfg = self._torch, self.config
@@ -439,6 +459,8 @@ class TensorNet:
                 raise ValidationError(f"length mismatch: {n} positions but {tuple(batch_t.shape)} batch codes")
             if n_samples is None:
                 n_samples = int(batch_t[-1]) + 1
+            if check:
+                self._batch_checked(batch_t, n, n_samples, remember=isinstance(batch, torch.Tensor))
         box_obj = self._as_box(box)
         capacity = self._capacity_hint.get((n, n_samples), self.neighbor_capacity(n))
         proj = self._species_checked(z_t, n, check, remember=isinstance(z, torch.Tensor))
@@ -527,6 +549,10 @@ class TensorNet:
                 f"model expects ({self.config.cutoff_lower}, {self.config.cutoff_upper})")
         if not neighbors.on_device or neighbors.row_ptr is None:
             raise ValidationError("evaluate() needs a device neighbor list from build_neighbor_list")
+        if not spec.deterministic:
+            # k_edge_rev bisects the sender's row by column, which needs rows sorted by sender
+            raise ValidationError(
+                "TensorNet needs rows sorted by sender: build the list with deterministic=True")
         dev = self.device
         n, ns, cap = system.n_atoms, system.n_samples, neighbors.capacity
         z = torch.as_tensor(np.ascontiguousarray(system.species, dtype=np.int32)).to(dev)

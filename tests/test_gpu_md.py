@@ -126,6 +126,24 @@ def test_drop_in_step_matches_oracle_with_device_forces():
     assert state.time_fs == pytest.approx(2.1)
 
 
+def test_composed_potentials_the_device_loop_cannot_integrate_are_refused():
+    """The reference integrates evaluate_auto of the whole composed potential (md.py:107-111); the
+    device loop runs the network's step only, so priors / derivative=False / no network raise."""
+    rng = np.random.default_rng(3)
+    system = P.build_system(rng.uniform(0, 5, (10, 3)), rng.choice([1, 6, 8], 10))
+    model = small_model()
+    state = P.initialize_state(system, 250.0, seed=1)
+    ok = P.langevin_middle_step(state, P.ComposedPotential(network=model), 0.5, 250.0, 1.0)
+    assert ok.time_fs == pytest.approx(0.5)
+    with pytest.raises(P.ValidationError, match="priors"):
+        P.langevin_middle_step(state, P.ComposedPotential(network=model, priors=P.PriorStack((P.ZBL(),))),
+                               0.5, 250.0, 1.0)
+    with pytest.raises(P.ValidationError, match="prior-only"):
+        P.run_simulation(state, P.ComposedPotential(priors=P.PriorStack((P.ZBL(),)), cutoff=4.0), 2, 0.5, 250.0, 1.0)
+    with pytest.raises(P.ValidationError, match="derivative"):
+        P.run_simulation(state, P.ComposedPotential(network=model, derivative=False), 2, 0.5, 250.0, 1.0)
+
+
 def test_run_simulation_frames_determinism_and_energy_conservation():
     rng = np.random.default_rng(2)
     pos = rng.uniform(0, 6, (24, 3))

@@ -226,6 +226,8 @@ def test_full_size_sweep_point_properties():
     assert half.count == ref.count
     hp = half.pairs[: half.count].cpu().numpy()
     assert np.array_equal(hp, ref.pairs[: ref.count])
+    assert np.array_equal(half.deltas[: half.count].cpu().numpy(), ref.deltas[: ref.count])      # bit-exact float64
+    assert np.array_equal(half.distances[: half.count].cpu().numpy(), ref.distances[: ref.count])
     full = P.build_neighbor_list(system, P.NeighborSpec(cutoff_upper=5.0, capacity=64 * n, strategy="cell",
                                                         full_list=True))
     assert full.count == 2 * half.count
@@ -233,6 +235,23 @@ def test_full_size_sweep_point_properties():
     assert rp[0] == 0 and rp[-1] == full.count and np.all(np.diff(rp) >= 0)
     fp = full.pairs[: full.count].cpu().numpy()
     assert np.array_equal(fp[:, 0], np.repeat(np.arange(n), np.diff(rp)))
+
+
+def test_one_million_atoms_bit_exact():
+    """1 048 576 atoms (the largest point of config B's sweep): pairs, deltas and distances of the
+    half list equal the C oracle's bit for bit (the oracle needs a few seconds on one core)."""
+    n = 1048576
+    _, pos, batch, box = synth.config_b_cloud(n, seed=0)
+    system = make_system(pos, batch, box)
+    nl = P.build_neighbor_list(system, P.NeighborSpec(cutoff_upper=5.0, capacity=32 * n, strategy="cell"))
+    ref = O.build_neighbor_list(pos, batch, box, 5.0, 32 * n, strategy="cell")
+    c = ref.count
+    assert nl.count == c
+    assert np.array_equal(nl.pairs[:c].cpu().numpy(), ref.pairs[:c])
+    assert np.array_equal(nl.deltas[:c].cpu().numpy(), ref.deltas[:c])
+    assert np.array_equal(nl.distances[:c].cpu().numpy(), ref.distances[:c])
+    tail = nl.pairs[c:]
+    assert bool((tail == -1).all()) and bool((nl.distances[c:] == 0).all())
 
 
 def test_nondeterministic_lists_hold_the_same_rows_grouped_by_receiver(rng):

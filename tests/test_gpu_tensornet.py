@@ -227,6 +227,32 @@ def test_evaluate_call_shapes_and_validation(rng):
         model(zn, pos.astype(np.float32), batch)
 
 
+def test_unsorted_lists_and_bad_batches_are_refused(rng):
+    """evaluate() bisects rows by sender, so a deterministic=False list is rejected; forward(check=True)
+    validates the sample codes the way build_system does in the reference."""
+    z, pos, batch, _ = small_open(rng, 24)
+    model = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)
+    system = P.build_system(pos, z, batch=batch)
+    loose = P.build_neighbor_list(system, P.NeighborSpec(cutoff_upper=4.0, capacity=2000, full_list=True,
+                                                         include_self_loops=True, deterministic=False))
+    with pytest.raises(P.ValidationError, match="sorted by sender"):
+        model.evaluate(system, loose)
+    zt, pt = torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32)
+    bad = batch.copy()
+    bad[3] = 1                                     # 0 0 0 1 0 ...: decreasing
+    with pytest.raises(P.ValidationError, match="non-decreasing"):
+        model(zt, pt, torch.as_tensor(bad))
+    with pytest.raises(P.ValidationError, match="n_samples"):
+        model(zt, pt, torch.as_tensor(batch), n_samples=1)
+    with pytest.raises(P.ValidationError, match="n_samples"):
+        model(zt, pt, torch.as_tensor(batch - 1))
+    # gaps (empty samples) are fine: energies of the empty samples are zero
+    e, _ = model(zt, pt, torch.as_tensor(batch * 2))
+    e0, _ = model(zt, pt, torch.as_tensor(batch))
+    assert e.shape == (3,) and float(e[1]) == 0.0
+    assert torch.equal(e[[0, 2]], e0)
+
+
 def test_invariances_on_device(rng):
     z, pos, batch, _ = small_open(rng, 26)
     model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=2)

@@ -55,6 +55,12 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     z, pos, batch, _ = synth.config_d_molecules(41, seed=3)
     e, f = sharding.evaluate_sharded(fake_step, z, pos, batch, None, device="cpu")
+    # the resident form used by bench.py (buffers allocated once, all_gather_into_tensor)
+    z_l, pos_l, b_l, _ = sharding.local_shard(z, pos, batch, rank, world)
+    gather = sharding.ResidentGather(batch, world, rank, "cpu")
+    for _ in range(2):
+        e2, f2 = gather(*fake_step(z_l, pos_l, b_l, None))
+    assert torch.equal(e, e2) and torch.equal(f, f2)
     if rank == 0:
         torch.save((e, f), out)
     dist.destroy_process_group()
