@@ -167,7 +167,10 @@ typedef struct nnp_tn_model {
        multiply-adds instead of ~60 per channel.  Needs num_rbf == 32; steps with more than four
        species fall back to the per-channel kernel on the device. */
     int32_t embed_projection;
-    int32_t reserved0;
+    /* GEMM engine of this model's calls: 0 = the library default (nnp_set_gemm_mode), 5 = streaming
+       tcgen05 mixes, 3 = per-tile tcgen05, 1 = mma.sync, 8 = FP32 FFMA.  Carried by the model so that
+       concurrent callers (threads, devices) do not share a mode switch. */
+    int32_t gemm_mode;
     const float *dp_wT;                                 /* [3][num_rbf][C] */
     const float *dp_b;                                  /* [3][C] */
     const float *rbf_means, *rbf_betas;                 /* [num_rbf] (radial.py:62-73) */

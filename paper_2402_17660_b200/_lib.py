@@ -76,7 +76,7 @@ class TnModel(ctypes.Structure):
         ("h1_w", GemmWeight), ("h1_wT", GemmWeight),
         ("lin_b", _p), ("h1_b", _p),
         ("h2_w", _p),
-        ("embed_projection", _i32), ("reserved0", _i32),
+        ("embed_projection", _i32), ("gemm_mode", _i32),
         ("dp_wT", _p), ("dp_b", _p), ("rbf_means", _p), ("rbf_betas", _p),
     ]
 

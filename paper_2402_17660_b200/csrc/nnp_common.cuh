@@ -30,7 +30,9 @@ void nnp_set_error(const char *fmt, ...);
     } while (0)
 
 // ---- launch accounting and per-kernel timing (test/bench instrumentation)
-extern int g_nnp_launch_count;
+// (thread-local: a caller's counters and profile session are its own; the library keeps no
+//  process-wide mutable state besides the default GEMM engine, which is an atomic)
+extern thread_local int g_nnp_launch_count;
 // wraps the grid argument of every launch: counts kernels enqueued by this library
 #define NNP_GRID(x) (++g_nnp_launch_count, (x))
 
@@ -44,6 +46,38 @@ struct NnpProfScope {
     ~NnpProfScope() { nnp_prof_mark(label, stream, 0); }
 };
 #define NNP_PROF(label, stream) NnpProfScope nnp_prof_scope_##__LINE__(label, stream)
+
+// Per-device one-time setup (cudaFuncSetAttribute is per device): `first(dev)` is true exactly
+// once per device ordinal for each static instance, from whichever thread gets there first.
+#include <atomic>
+struct NnpPerDeviceOnce {
+    std::atomic<unsigned long long> done[2];
+    bool first(int dev)
+    {
+        if (dev < 0 || dev >= 128) return true;    // unknown ordinal: just redo the setup
+        const unsigned long long bit = 1ull << (dev & 63);
+        return (done[dev >> 6].fetch_or(bit) & bit) == 0;
+    }
+};
+static inline int nnp_current_device()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+static inline int nnp_sm_count()
+{
+    static std::atomic<int> sms[128];
+    const int dev = nnp_current_device();
+    if (dev < 0 || dev >= 128) return 148;
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        sms[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
 
 static inline size_t nnp_align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

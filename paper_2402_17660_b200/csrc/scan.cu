@@ -16,7 +16,7 @@ void nnp_set_error(const char *fmt, ...)
 
 extern "C" const char *nnp_last_error(void) { return g_last_error; }
 
-int g_nnp_launch_count = 0;
+thread_local int g_nnp_launch_count = 0;
 extern "C" int nnp_launch_count(int reset)
 {
     int v = g_nnp_launch_count;
@@ -33,8 +33,8 @@ struct ProfRec {
     const char *label;
     cudaEvent_t start, stop;
 };
-bool g_prof_on = false;
-std::vector<ProfRec> g_prof_recs;
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfRec> g_prof_recs;
 }  // namespace
 
 void nnp_prof_mark(const char *label, cudaStream_t stream, int begin)

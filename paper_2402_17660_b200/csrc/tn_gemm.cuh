@@ -294,5 +294,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
     }
 }
 
-extern int g_nnp_gemm_use_mma;  // 5 = streaming tcgen05 for the 128 x 128 mixes, per-tile tcgen05 otherwise (default);
-                                // 3 = per-tile tcgen05 3xTF32; 1 = mma.sync 3xTF32; 0 = FP32 FFMA
+// GEMM engine of the calling thread's current library call (set at every entry point from the
+// model's gemm_mode, else from the process default of nnp_set_gemm_mode):
+// 5 = streaming tcgen05 for the 128 x 128 mixes, per-tile tcgen05 otherwise (default);
+// 3 = per-tile tcgen05 3xTF32; 1 = mma.sync 3xTF32; 0 = FP32 FFMA
+extern thread_local int t_nnp_gemm_mode;

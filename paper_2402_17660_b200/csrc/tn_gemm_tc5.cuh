@@ -636,14 +636,10 @@ static int launch_stream(const GemmBatch &b, int count, cudaStream_t stream)
             (int64_t)b.g[i].M * 9 * b.g[i].ldo >= (int64_t)1 << 31)
             return -100;
     constexpr int smem = ST_STAGES * ST_STAGE_BYTES + 1024;
-    static int num_sms = 0;
-    if (num_sms == 0) {
+    static NnpPerDeviceOnce once;
+    if (once.first(nnp_current_device()))
         cudaFuncSetAttribute(gemm_stream_kernel<PRO, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
+    const int num_sms = nnp_sm_count();
     int tiles[3] = {0, 0, 0}, total = 0;
     for (int i = 0; i < count; ++i) {
         tiles[i] = (b.g[i].M + BM - 1) / BM;
@@ -670,12 +666,10 @@ template <int PRO, int EPI, int NT>
 static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStream_t stream)
 {
     const int smem = 2 * BM * 128 + 2 * NT * 128 + 1024;
-    static bool configured = false;
-    if (!configured) {
+    static NnpPerDeviceOnce once;
+    if (once.first(nnp_current_device()))
         cudaFuncSetAttribute(gemm_nt_tc5_kernel<PRO, EPI, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
     dim3 grid(NNP_GRID((maxM + BM - 1) / BM), (maxN + NT - 1) / NT, count);
     gemm_nt_tc5_kernel<PRO, EPI, NT><<<grid, THREADS, smem, stream>>>(b);
     NNP_CHECK_LAUNCH("gemm_nt_tc5");
@@ -724,15 +718,15 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
     // (measured at 2 489 atoms: 0.15 vs 0.24 ms for the eight dense GEMMs)
     const bool streamable = maxN == 128 && b.g[0].K == 128;
     static const int dense_tiny_m = getenv("NNP_DENSE_TINY_M") ? atoi(getenv("NNP_DENSE_TINY_M")) : 8192;
-    const bool tiny = g_nnp_gemm_use_mma == 5 && (maxM <= 1024 || (!streamable && maxM <= dense_tiny_m));
-    if (g_nnp_gemm_use_mma >= 2 && !tiny) {
+    const bool tiny = t_nnp_gemm_mode == 5 && (maxM <= 1024 || (!streamable && maxM <= dense_tiny_m));
+    if (t_nnp_gemm_mode >= 2 && !tiny) {
         int rc = -100;
-        if (g_nnp_gemm_use_mma == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);
+        if (t_nnp_gemm_mode == 5) rc = tc5::launch_stream<PRO, EPI>(b, count, stream);
         if (rc == -100) rc = tc5::launch<PRO, EPI>(b, count, stream);
         if (rc != -100) return rc;
     }
     dim3 grid(NNP_GRID((maxM + GEMM_BM - 1) / GEMM_BM), (maxN + GEMM_BN - 1) / GEMM_BN, count);
-    if (g_nnp_gemm_use_mma)
+    if (t_nnp_gemm_mode)
         gemm_nt_kernel<PRO, EPI, true><<<grid, GEMM_THREADS, 0, stream>>>(b);
     else
         gemm_nt_kernel<PRO, EPI, false><<<grid, GEMM_THREADS, 0, stream>>>(b);

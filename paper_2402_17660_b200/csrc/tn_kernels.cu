@@ -23,8 +23,10 @@
 #include "tn_gemm_tc5.cuh"
 #include "tn_math.cuh"
 
-int g_nnp_gemm_use_mma = 5;  // 5 = streaming tcgen05 for the 128x128 mixes (default; other shapes use 3),
-                              // 3 = tcgen05 one tile per CTA, 1 = mma.sync, 0 = FFMA
+#include <atomic>
+thread_local int t_nnp_gemm_mode = 5;
+static std::atomic<int> g_gemm_default{5};   // nnp_set_gemm_mode: 5 = streaming tcgen05 for the 128x128 mixes
+                                             // (other shapes use 3), 3 = tcgen05 one tile per CTA, 1 = mma.sync, 0 = FFMA
 
 namespace {
 
@@ -1366,6 +1368,8 @@ int validate_model(const nnp_tn_model *m)
                   "channels must be 32, 64 or 128");
     NNP_CHECK_ARG(m->num_layers >= 0 && m->num_layers <= NNP_TN_MAX_LAYERS, "num_layers out of range");
     NNP_CHECK_ARG(m->num_knots >= 2, "num_knots must be >= 2");
+    NNP_CHECK_ARG(m->gemm_mode == 0 || m->gemm_mode == 1 || m->gemm_mode == 3 || m->gemm_mode == 5 || m->gemm_mode == 8,
+                  "gemm_mode must be 0 (default), 1, 3, 5 or 8");
     NNP_CHECK_ARG(m->u_step > 0.0f, "u_step must be positive");
     NNP_CHECK_ARG(m->cutoff_lower >= 0.0f && m->cutoff_lower < m->cutoff_upper, "bad cutoffs");
     NNP_CHECK_ARG(!m->embed_projection || (m->num_rbf == EMB_K && m->channels == EMB_SLOTS * EMB_K && m->dp_wT && m->dp_b && m->rbf_means &&
@@ -1640,6 +1644,8 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
     d.forces = forces;
     d.per_atom = per_atom;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    t_nnp_gemm_mode = m->gemm_mode == 0 ? g_gemm_default.load(std::memory_order_relaxed)
+                                        : (m->gemm_mode == 8 ? 0 : m->gemm_mode);
     switch (m->channels) {
     case 32: return run_step<32>(d, st);
     case 64: return run_step<64>(d, st);
@@ -1649,7 +1655,7 @@ extern "C" int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int3
 
 extern "C" int nnp_set_gemm_mode(int use_mma)
 {
-    g_nnp_gemm_use_mma = (use_mma == 5 || use_mma == 3 || use_mma == 1) ? use_mma : (use_mma <= 0 ? 0 : 5);
+    g_gemm_default.store((use_mma == 5 || use_mma == 3 || use_mma == 1) ? use_mma : (use_mma <= 0 ? 0 : 5));
     return NNP_OK;
 }
 
@@ -1660,5 +1666,6 @@ extern "C" int nnp_test_gemm_nt(const float *A, const nnp_gemm_weight *W, const 
                   "bad arguments to nnp_test_gemm_nt");
     GemmBatch b{};
     b.g[0] = plain_gemm(A, *W, bias, out, M, N, K);
+    t_nnp_gemm_mode = g_gemm_default.load(std::memory_order_relaxed);
     return gemm_launch<PRO_NONE, EPI_STORE>(b, 1, static_cast<cudaStream_t>(stream));
 }

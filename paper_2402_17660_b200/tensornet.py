@@ -193,7 +193,7 @@ class TensorNet:
 
     def __init__(self, config: Optional[TNConfig] = None, params: Optional[Dict[str, np.ndarray]] = None,
                  seed: int = 0, device="cuda", use_graph: bool = True, strategy: str = "auto",
-                 embed_projection: Optional[bool] = None, **config_kwargs):
+                 embed_projection: Optional[bool] = None, gemm_mode: int = 0, **config_kwargs):
         torch = _lib.require_cuda()
         self._torch = torch
         self.lib = _lib.load()
@@ -207,6 +207,9 @@ class TensorNet:
         self.use_graph = use_graph
         self.strategy = strategy
         self.embed_projection = embed_projection
+        if gemm_mode not in (0, 1, 3, 5, 8):
+            raise ValidationError("gemm_mode must be 0 (library default), 5, 3, 1 or 8 (FFMA)")
+        self.gemm_mode = gemm_mode      # per model, so concurrent models do not share a switch
         self._plans: Dict[tuple, _Plan] = {}
         self._last_plan: Optional[_Plan] = None
         self._z_key, self._z_proj = None, False
@@ -270,6 +273,7 @@ class TensorNet:
         if self.embed_projection and not self._proj_capable:
             raise ValidationError("embed_projection needs embedding_dimension=128 and num_rbf=32")
         m.embed_projection = 0          # set per step from the plan (see _use_projection)
+        m.gemm_mode = self.gemm_mode
         m.dp_wT = dev("dp_wT", np.transpose(P["dp_w"], (0, 2, 1)))      # [3][K][C]
         m.dp_b = dev("dp_b", P["dp_b"])
         m.rbf_means, m.rbf_betas = dev("rbf_means", P["rbf_means"]), dev("rbf_betas", P["rbf_betas"])

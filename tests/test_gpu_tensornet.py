@@ -253,6 +253,46 @@ def test_unsorted_lists_and_bad_batches_are_refused(rng):
     assert torch.equal(e[[0, 2]], e0)
 
 
+def test_gemm_engine_is_per_model_and_thread_safe(rng):
+    """The GEMM engine travels in the model struct (nnp_tn_model.gemm_mode), not in a process
+    global: two models with different engines evaluated from two threads at once give exactly
+    what each gives alone, and the same as the library-wide switch gives."""
+    import threading
+
+    z, pos, batch, _ = small_open(rng, 40)
+    args = (torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32), torch.as_tensor(batch))
+    kw = dict(embedding_dimension=64, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1,
+              use_graph=False)
+    ffma, mma = P.TensorNet(gemm_mode=8, **kw), P.TensorNet(gemm_mode=1, **kw)
+    plain = P.TensorNet(**kw)
+    alone = {"ffma": ffma(*args), "mma": mma(*args)}
+    for mode, key in ((0, "ffma"), (1, "mma")):
+        _lib.load().nnp_set_gemm_mode(mode)
+        try:
+            e, f = plain(*args)
+        finally:
+            _lib.load().nnp_set_gemm_mode(_lib.DEFAULT_GEMM_MODE)
+        assert torch.equal(e, alone[key][0]) and torch.equal(f, alone[key][1])
+    out = {}
+
+    def work(name, model):
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for _ in range(20):
+                out[name] = model(*args)
+            torch.cuda.current_stream().synchronize()
+
+    threads = [threading.Thread(target=work, args=(n, m)) for n, m in (("ffma", ffma), ("mma", mma))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for key in ("ffma", "mma"):
+        assert torch.equal(out[key][0], alone[key][0]) and torch.equal(out[key][1], alone[key][1])
+    with pytest.raises(P.ValidationError, match="gemm_mode"):
+        P.TensorNet(gemm_mode=2, **kw)
+
+
 def test_invariances_on_device(rng):
     z, pos, batch, _ = small_open(rng, 26)
     model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=2)

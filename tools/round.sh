@@ -1,7 +1,7 @@
 #!/bin/bash
-# One GPU call: parity tests, smoke, bench (all workloads), ncu launch list.
+# One GPU call: parity tests, smoke, bench (all workloads), ncu launch list.  $1 = extra pytest args
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 -p no:cacheprovider $1 > gpurun_out/pytest_gpu.log 2>&1
 tail -5 gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py smoke 2>&1 | tail -3
 bash tools/bench.sh
