@@ -64,11 +64,14 @@ __device__ __forceinline__ void stv(float *p, const float (&v)[CPL])
 }
 
 constexpr int NNP_PARTS = 4;  // max channel parts a node's row is split over (C / (32 * CPL))
+constexpr int NNP_GD_SLOTS = 8;
 
 struct TnDev {
     nnp_tn_model m;
     int n, n_samples, capacity;
-    int nparts;  // channel-part slots of g_d / g_u in use this step (<= NNP_PARTS)
+    int nparts;  // channel-part slots of g_u in use this step (<= NNP_PARTS)
+    int gd_slots;  // g_d slots per writing kernel (<= NNP_GD_SLOTS): channel parts, times two when the
+                   // reverse message kernel runs as two warps (I+A | S) per receiver
     // inputs
     const int *species, *batch, *order, *row_ptr, *pairs, *nl_counts;
     const float *deltas, *dists;
@@ -78,7 +81,16 @@ struct TnDev {
     int *col, *rev, *newpos;
     float4 *geoA;  // (table coordinate, phi, dphi/dd, 1/d)
     float4 *geoB;  // (ux, uy, uz, u = exp(cutoff_lower - d))
-    float *g_d;    // [(L+1) * nparts][capacity] dE/dd_e: one slot per (writing kernel, channel part), so every
+    // per-edge records of the interaction layers' row walkers, fixed for the whole step (every layer
+    // of both sweeps reads them): sender and knot interval, and the four cubic-Hermite weights of
+    // the interval's two knots, already multiplied by the cosine envelope and stored in the order
+    // (even knot value, even knot slope, odd knot value, odd knot slope) - the walkers keep the
+    // even-numbered and the odd-numbered knot of their current interval in two fixed register sets,
+    // so moving to the next interval replaces one set and never moves data between registers.
+    int2 *ejk;     // (sender j, knot interval kn)
+    float4 *hwV;   // weights of f_e * phi_e
+    float4 *hwD;   // weights of d(f_e * phi_e)/dd = f' * dtx/dd * phi + f * phi'
+    float *g_d;    // [(L+1) * gd_slots][capacity] dE/dd_e: one slot per (writing kernel, channel part), so every
                    // kernel stores its share without a read-modify-write; summed in k_forces
     float4 *g_u;   // [NNP_PARTS][capacity] dE/du_e
     // workspace: nodes
@@ -125,6 +137,14 @@ __global__ void k_prep_nodes(TnDev d)
         for (int c = b + 1; c <= d.n_samples; ++c) d.sample_ptr[c] = d.n;
 }
 
+__device__ __forceinline__ int knot_of(float tx, int num_knots, float &t)
+{
+    int kn = (int)tx;
+    kn = kn > num_knots - 2 ? num_knots - 2 : kn;
+    t = tx - (float)kn;
+    return kn;
+}
+
 // Per-edge geometry shared by every layer of the forward and reverse sweeps, written in the
 // MODEL's edge order: each receiver's row is re-sorted by decreasing distance (= increasing table
 // coordinate), so that consecutive edges of a row fall into the same or the next knot interval
@@ -169,10 +189,23 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
         d.newpos[e] = p;
         d.col[p] = j;
         d.geoA[p] = make_float4(tx, phi, dphi, invd);
+        {
+            float t;
+            const int kn = knot_of(tx, d.m.num_knots, t);
+            const Hermite h = hermite_weights(t);
+            const float su = -u / d.m.u_step * phi;            // d(table coordinate)/dd, times the envelope
+            const float l0 = h.h00 * phi, l1 = h.h10 * phi, r0 = h.h01 * phi, r1 = h.h11 * phi;
+            const float dl0 = fmaf(h.d00, su, h.h00 * dphi), dl1 = fmaf(h.d10, su, h.h10 * dphi);
+            const float dr0 = fmaf(h.d01, su, h.h01 * dphi), dr1 = fmaf(h.d11, su, h.h11 * dphi);
+            const bool even = (kn & 1) == 0;                   // the interval's left knot is the even one
+            d.ejk[p] = make_int2(j, kn);
+            d.hwV[p] = even ? make_float4(l0, l1, r0, r1) : make_float4(r0, r1, l0, l1);
+            d.hwD[p] = even ? make_float4(dl0, dl1, dr0, dr1) : make_float4(dr0, dr1, dl0, dl1);
+        }
         d.geoB[p] = make_float4(d.deltas[3 * (size_t)e] * invd, d.deltas[3 * (size_t)e + 1] * invd,
                                 d.deltas[3 * (size_t)e + 2] * invd, u);
         for (int q = 0; q < d.nparts; ++q) d.g_u[(size_t)q * d.capacity + p] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int q = 0; q < d.nparts * (d.m.num_layers + 1); ++q) d.g_d[(size_t)q * d.capacity + p] = 0.0f;
+        for (int q = 0; q < d.gd_slots * (d.m.num_layers + 1); ++q) d.g_d[(size_t)q * d.capacity + p] = 0.0f;
     }
 }
 
@@ -196,13 +229,6 @@ __global__ void k_edge_rev(TnDev d)
 // radial functions, [knot][value|slope][3][C] (`tables`, for row walkers that keep the two knots of
 // their current interval in registers), and per knot interval the monomial coefficients
 // (`tables_mono`, Horner form for kernels that visit intervals in no particular order).
-__device__ __forceinline__ int knot_of(float tx, int num_knots, float &t)
-{
-    int kn = (int)tx;
-    kn = kn > num_knots - 2 ? num_knots - 2 : kn;
-    t = tx - (float)kn;
-    return kn;
-}
 
 // Lookup of the 3 radial functions of `CPL` channels: value f[k][v] and d f / d(knot coordinate).
 // The host stores, per knot interval, the cubic's monomial coefficients [c0 c1 c2 c3][3][C]
@@ -508,12 +534,14 @@ __global__ void k_embed_gate_bwd(const float *__restrict__ GX, const float *__re
 }
 
 // ----------------------------------------------------------------------- interaction edges
-// The two knots of a row walker's current table interval, for the radial functions [K0, K0 + NG):
-// rows are sorted by table coordinate, so moving on means "same interval" (no load), "next
-// interval" (one knot) or a jump (two knots) - a warp-uniform decision.
+// The two knots of a row walker's current table interval, for the radial functions [K0, K0 + NG),
+// held in two fixed register sets: the even-numbered knot and the odd-numbered knot.  Rows are
+// sorted by table coordinate, so moving on means "same interval" (nothing), "next interval" (one
+// knot replaces the one that fell behind - no register moves, the per-edge weights of k_edge_order
+// already come in (even, odd) order) or a jump (both knots) - a warp-uniform decision.
 template <int C, int CPL, int K0, int NG>
-struct KnotCacheG {
-    float v0[NG][CPL], m0[NG][CPL], v1[NG][CPL], m1[NG][CPL];
+struct KnotEO {
+    float ev[NG][CPL], em[NG][CPL], ov[NG][CPL], om[NG][CPL];
     int kn;
     __device__ __forceinline__ void init() { kn = -4; }
     __device__ __forceinline__ static void load_knot(const float *__restrict__ tab, int knot, int cb,
@@ -529,31 +557,22 @@ struct KnotCacheG {
     __device__ __forceinline__ void seek(const float *__restrict__ tab, int k, int cb)
     {
         if (k == kn) return;
-        if (k == kn + 1) {
-#pragma unroll
-            for (int q = 0; q < NG; ++q)
-#pragma unroll
-                for (int v = 0; v < CPL; ++v) {
-                    v0[q][v] = v1[q][v];
-                    m0[q][v] = m1[q][v];
-                }
+        const bool jump = k != kn + 1;
+        if (k & 1) {                       // left knot k is odd, right knot k + 1 even
+            if (jump) load_knot(tab, k, cb, ov, om);
+            load_knot(tab, k + 1, cb, ev, em);
         } else {
-            load_knot(tab, k, cb, v0, m0);
+            if (jump) load_knot(tab, k, cb, ev, em);
+            load_knot(tab, k + 1, cb, ov, om);
         }
-        load_knot(tab, k + 1, cb, v1, m1);
         kn = k;
     }
-    __device__ __forceinline__ void value(const Hermite &h, int k, float (&f)[CPL]) const
+    // w = the edge's four weights in (even value, even slope, odd value, odd slope) order
+    __device__ __forceinline__ void eval(const float4 &w, int k, float (&f)[CPL]) const
     {
 #pragma unroll
         for (int v = 0; v < CPL; ++v)
-            f[v] = fmaf(h.h00, v0[k][v], fmaf(h.h10, m0[k][v], fmaf(h.h01, v1[k][v], h.h11 * m1[k][v])));
-    }
-    __device__ __forceinline__ void slope(const Hermite &h, int k, float (&df)[CPL]) const
-    {
-#pragma unroll
-        for (int v = 0; v < CPL; ++v)
-            df[v] = fmaf(h.d00, v0[k][v], fmaf(h.d10, m0[k][v], fmaf(h.d01, v1[k][v], h.d11 * m1[k][v])));
+            f[v] = fmaf(w.x, ev[k][v], fmaf(w.y, em[k][v], fmaf(w.z, ov[k][v], w.w * om[k][v])));
     }
 };
 
@@ -569,31 +588,24 @@ __device__ __forceinline__ void message_row_part(const TnDev &d, const float *__
 #pragma unroll
         for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
     const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
-    KnotCacheG<C, CPL, K0, NG> kc;
+    KnotEO<C, CPL, K0, NG> kc;
     kc.init();
-    const int nk = d.m.num_knots;
-    int j = e0 < e1 ? d.col[e0] : 0;
-    float4 ga = e0 < e1 ? d.geoA[e0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int2 *__restrict__ ejk = d.ejk;
+    const float4 *__restrict__ hwV = d.hwV;
+    const float *ybase = Y + Q0 * C + cb;
+    int2 jk = e0 < e1 ? __ldg(ejk + e0) : make_int2(0, 0);
     for (int e = e0; e < e1; ++e) {
-        const float *yj = Y + ((size_t)j * 9 + Q0) * C + cb;
+        const float *yj = ybase + (size_t)jk.x * (9 * C);
         float y[NQ][CPL];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) ldv<CPL>(yj + q * C, y[q]);
-        float t;
-        const int kn = knot_of(ga.x, nk, t);
-        kc.seek(tab, kn, cb);
-        const float phi = ga.y;
-        if (e + 1 < e1) {
-            j = d.col[e + 1];
-            ga = d.geoA[e + 1];
-        }
-        const Hermite h = hermite_weights(t);
+        const float4 wc = __ldg(hwV + e);       // lands together with the gathered row
+        kc.seek(tab, jk.y, cb);
+        if (e + 1 < e1) jk = __ldg(ejk + e + 1);
 #pragma unroll
         for (int k = 0; k < NG; ++k) {
             float f[CPL];
-            kc.value(h, k, f);
-#pragma unroll
-            for (int v = 0; v < CPL; ++v) f[v] *= phi;
+            kc.eval(wc, k, f);
             // local component range of group K0 + k
             const int g = K0 + k;
             const int qa = (g == 0 ? 0 : (g == 1 ? 1 : 4)) - Q0, qb = (g == 0 ? 1 : (g == 1 ? 4 : 9)) - Q0;
@@ -613,7 +625,7 @@ __device__ __forceinline__ void message_row_part(const TnDev &d, const float *__
 // knot data and accumulators in registers.  The node update Q = (M*Y + Y*M)/(|.|^2 + 1) follows
 // after a block barrier, the two warps taking half of the lane's channels each.
 template <int C, int CPL>
-__global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
+__global__ void __launch_bounds__(128, 5) k_edge_message_split(TnDev d, int layer)
 {
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
@@ -664,6 +676,341 @@ __global__ void __launch_bounds__(256) k_edge_message_split(TnDev d, int layer)
     float *qo = d.Qc + (size_t)s * 9 * C + cq;
 #pragma unroll
     for (int q = 0; q < 9; ++q) stv<HC>(qo + q * C, qv[q]);
+}
+
+// The same reverse edge op as k_edge_message_bwd below (see there for the formulas), run like the
+// forward kernel: two warps per (receiver, channel part) - one owns the I and A components, the other
+// the S components - each walking the distance-sorted row with the interval's two knots in registers
+// and the per-edge Hermite weights of k_edge_order (hwV for f*phi, hwD for d(f*phi)/dd), so no table
+// coefficient is loaded per edge.  The per-edge sum over channels is collected eight edges at a time:
+// every lane keeps its partial of eight edges and one transposing butterfly (7 + 2 shuffles) leaves
+// the eight totals in lanes 0, 4, ..., 28, which store them side by side.
+template <int C, int CPL, int K0, int NG, int Q0, int NQ>
+__device__ __forceinline__ void message_bwd_row_part(const TnDev &d, const float *__restrict__ tab,
+                                                     const float *__restrict__ GM, float *__restrict__ GY,
+                                                     const float *__restrict__ Yown, float *__restrict__ gd_slot,
+                                                     int s, int cb)
+{
+    const int lane = threadIdx.x & 31;
+    // wy[q] = weight of gathered component q in <G_M[b], Yc[a]> of its group (metric folded in):
+    // I: 3 y0 ; A: 2 y_q ; S: 2 y4 + y5, 2 y5 + y4, 2 y_q
+    float wy[NQ][CPL], acc[NQ][CPL];
+    {
+        const float *p = Yown + ((size_t)s * 9 + Q0) * C + cb;
+        const float *py = GY + ((size_t)s * 9 + Q0) * C + cb;
+        float y[NQ][CPL];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            ldv<CPL>(p + q * C, y[q]);
+            ldv<CPL>(py + q * C, acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) {
+                const int gq = Q0 + q;
+                wy[q][v] = gq == 0 ? 3.0f * y[q][v]
+                         : gq == 4 ? 2.0f * y[q][v] + y[q + (gq == 4 ? 1 : 0)][v]
+                         : gq == 5 ? 2.0f * y[q][v] + y[q - (gq == 5 ? 1 : 0)][v]
+                                   : 2.0f * y[q][v];
+            }
+    }
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    KnotEO<C, CPL, K0, NG> kc;
+    kc.init();
+    const int2 *__restrict__ ejk = d.ejk;
+    const float4 *__restrict__ hwV = d.hwV;
+    const float4 *__restrict__ hwD = d.hwD;
+    const float *gbase = GM + Q0 * C + cb;
+    // (measured: keeping the next edge's gather in flight while this edge is evaluated is SLOWER,
+    //  2.27 vs 1.31 ms per step - the knot loads of seek() complete behind the prefetched row)
+    int2 jk = e0 < e1 ? __ldg(ejk + e0) : make_int2(0, 0);
+    for (int eb = e0; eb < e1; eb += 8) {
+        float pb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            pb[i] = 0.0f;
+            if (eb + i < e1) {                       // warp-uniform
+                const float *gj = gbase + (size_t)jk.x * (9 * C);
+                float g[NQ][CPL];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) ldv<CPL>(gj + q * C, g[q]);
+                const float4 wvc = __ldg(hwV + eb + i), wdc = __ldg(hwD + eb + i);   // land with the gathered row
+                kc.seek(tab, jk.y, cb);
+                if (eb + i + 1 < e1) jk = __ldg(ejk + eb + i + 1);
+                float p = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NG; ++k) {
+                    float f[CPL], F[CPL], dk[CPL];
+                    kc.eval(wvc, k, f);
+                    kc.eval(wdc, k, F);
+                    const int gi = K0 + k;
+                    const int qa = (gi == 0 ? 0 : (gi == 1 ? 1 : 4)) - Q0, qb = (gi == 0 ? 1 : (gi == 1 ? 4 : 9)) - Q0;
+#pragma unroll
+                    for (int v = 0; v < CPL; ++v) dk[v] = 0.0f;
+#pragma unroll
+                    for (int q = qa; q < qb; ++q)
+#pragma unroll
+                        for (int v = 0; v < CPL; ++v) {
+                            acc[q][v] = fmaf(f[v], g[q][v], acc[q][v]);
+                            dk[v] = fmaf(g[q][v], wy[q][v], dk[v]);
+                        }
+#pragma unroll
+                    for (int v = 0; v < CPL; ++v) p = fmaf(dk[v], F[v], p);
+                }
+                pb[i] = p;
+            }
+        }
+        // eight warp sums at once: after the three transposing steps lane l holds (a quarter of) the
+        // total of edge ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1)
+#pragma unroll
+        for (int o = 16, h = 4; h >= 1; o >>= 1, h >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const float send = up ? pb[i] : pb[i + h];
+                const float keep = up ? pb[i + h] : pb[i];
+                pb[i] = keep + __shfl_xor_sync(NNP_FULL_MASK, send, o);
+            }
+        }
+        float tot = pb[0];
+        tot += __shfl_xor_sync(NNP_FULL_MASK, tot, 2);
+        tot += __shfl_xor_sync(NNP_FULL_MASK, tot, 1);
+        const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && eb + idx < e1 && __ldg(ejk + eb + idx).x != s) gd_slot[eb + idx] = tot;
+    }
+    float *out = GY + ((size_t)s * 9 + Q0) * C + cb;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+template <int C, int CPL>
+__global__ void __launch_bounds__(128, 4) k_edge_message_bwd_split(TnDev d, int layer, const float *GM,
+                                                                float *GY, float *gd_layer)
+{
+    constexpr int NPARTS = C / (32 * CPL);
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / (2 * NPARTS), rem = gw - s * (2 * NPARTS);
+    const int part = rem >> 1, half = rem & 1;
+    if (s >= d.n) return;
+    const int cb = part * 32 * CPL + lane * CPL;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    float *gd_slot = gd_layer + (size_t)(2 * part + half) * d.capacity;   // this warp's own slots
+    if (half == 0) message_bwd_row_part<C, CPL, 0, 2, 0, 4>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
+    else message_bwd_row_part<C, CPL, 2, 1, 4, 5>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
+}
+
+// ---- sender rows through a shared-memory ring fed by bulk asynchronous copies (TMA engine)
+// A block is one receiver (both component halves, all channel parts), so every warp of the block
+// needs the same sender row: one elected lane requests the whole 9 x C row of the edge RING_DEPTH
+// positions ahead with a single cp.async.bulk (global -> shared, completion counted on an mbarrier),
+// and the warps read their components from shared memory when the row has landed.  The L2 round
+// trip of the gather is then hidden behind RING_DEPTH edges of arithmetic instead of being paid per
+// edge by every warp (the register-gather version sits at 44 % issue utilisation waiting on
+// long-scoreboard stalls); the bytes that cross the L2 fabric are unchanged.
+// MEASURED (config C, profiles/r2_summary.md): 1.06 ms per launch against 0.65 ms for the register
+// gather - the bulk-copy path delivered 7.4 TB/s (19 B/clk/SM) where the LDG path reaches 16.7 TB/s,
+// and the mbarrier polls add 40 % instructions.  Kept selectable (NNP_BWD_SPLIT=2), not the default.
+constexpr int RING_DEPTH = 4;
+
+__device__ __forceinline__ uint32_t ring_smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ring_bar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ring_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void ring_bar_wait(uint64_t *bar, uint32_t parity)
+{
+    const uint32_t addr = ring_smem_u32(bar);
+    uint32_t done = 0;
+    for (long spin = 0; !done; ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (spin > (1L << 28)) __trap();   // never hang the device on a protocol error
+    }
+}
+__device__ __forceinline__ void ring_bar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ring_smem_u32(bar)) : "memory");
+}
+// request `bytes` (multiple of 16, both addresses 16-byte aligned) and announce them on `bar`
+__device__ __forceinline__ void ring_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    const uint32_t b = ring_smem_u32(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(ring_smem_u32(dst)), "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
+template <int C>
+struct RowRing {
+    float *rows;            // [RING_DEPTH][9 * C]
+    uint64_t *full, *empty; // [RING_DEPTH] each
+};
+
+template <int C, int CPL, int K0, int NG, int Q0, int NQ>
+__device__ __forceinline__ void message_bwd_row_ring(const TnDev &d, const float *__restrict__ tab,
+                                                     const float *__restrict__ GM, float *__restrict__ GY,
+                                                     const float *__restrict__ Yown, float *__restrict__ gd_slot,
+                                                     int s, int cb, const RowRing<C> &ring, bool producer)
+{
+    const int lane = threadIdx.x & 31;
+    float wy[NQ][CPL], acc[NQ][CPL];
+    {
+        const float *p = Yown + ((size_t)s * 9 + Q0) * C + cb;
+        const float *py = GY + ((size_t)s * 9 + Q0) * C + cb;
+        float y[NQ][CPL];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            ldv<CPL>(p + q * C, y[q]);
+            ldv<CPL>(py + q * C, acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) {
+                const int gq = Q0 + q;
+                wy[q][v] = gq == 0 ? 3.0f * y[q][v]
+                         : gq == 4 ? 2.0f * y[q][v] + y[q + (gq == 4 ? 1 : 0)][v]
+                         : gq == 5 ? 2.0f * y[q][v] + y[q - (gq == 5 ? 1 : 0)][v]
+                                   : 2.0f * y[q][v];
+            }
+    }
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    KnotEO<C, CPL, K0, NG> kc;
+    kc.init();
+    const int2 *__restrict__ ejk = d.ejk;
+    const float4 *__restrict__ hwV = d.hwV;
+    const float4 *__restrict__ hwD = d.hwD;
+    constexpr uint32_t ROW_BYTES = 9 * C * sizeof(float);
+    // prologue: the first RING_DEPTH rows are requested at once (their slots are free)
+    if (producer && lane == 0) {
+        for (int i = 0; i < RING_DEPTH && e0 + i < e1; ++i)
+            ring_bulk_load(ring.rows + i * (9 * C), GM + (size_t)__ldg(ejk + e0 + i).x * (9 * C), ROW_BYTES,
+                           ring.full + i);
+    }
+    int kn_next = e0 < e1 ? __ldg(ejk + e0).y : 0;
+    int j_ahead = (producer && e0 + RING_DEPTH < e1) ? __ldg(ejk + e0 + RING_DEPTH).x : 0;   // sender of edge e + RING_DEPTH
+    for (int eb = e0; eb < e1; eb += 8) {
+        float pb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            pb[i] = 0.0f;
+            if (eb + i < e1) {                       // warp-uniform
+                const int idx = eb + i - e0;
+                const int slot = idx % RING_DEPTH;
+                const uint32_t use = (uint32_t)(idx / RING_DEPTH);
+                const float4 wvc = __ldg(hwV + eb + i), wdc = __ldg(hwD + eb + i);
+                const int kn = kn_next;
+                kc.seek(tab, kn, cb);
+                if (eb + i + 1 < e1) kn_next = __ldg(ejk + eb + i + 1).y;
+                ring_bar_wait(ring.full + slot, use & 1u);
+                const float *gj = ring.rows + slot * (9 * C) + Q0 * C + cb;
+                float g[NQ][CPL];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    if constexpr (CPL == 4) {
+                        const float4 t = *reinterpret_cast<const float4 *>(gj + q * C);
+                        g[q][0] = t.x; g[q][1] = t.y; g[q][2] = t.z; g[q][3] = t.w;
+                    } else if constexpr (CPL == 2) {
+                        const float2 t = *reinterpret_cast<const float2 *>(gj + q * C);
+                        g[q][0] = t.x; g[q][1] = t.y;
+                    } else {
+                        g[q][0] = gj[q * C];
+                    }
+                }
+                float p = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NG; ++k) {
+                    float f[CPL], F[CPL], dk[CPL];
+                    kc.eval(wvc, k, f);
+                    kc.eval(wdc, k, F);
+                    const int gi = K0 + k;
+                    const int qa = (gi == 0 ? 0 : (gi == 1 ? 1 : 4)) - Q0, qb = (gi == 0 ? 1 : (gi == 1 ? 4 : 9)) - Q0;
+#pragma unroll
+                    for (int v = 0; v < CPL; ++v) dk[v] = 0.0f;
+#pragma unroll
+                    for (int q = qa; q < qb; ++q)
+#pragma unroll
+                        for (int v = 0; v < CPL; ++v) {
+                            acc[q][v] = fmaf(f[v], g[q][v], acc[q][v]);
+                            dk[v] = fmaf(g[q][v], wy[q][v], dk[v]);
+                        }
+#pragma unroll
+                    for (int v = 0; v < CPL; ++v) p = fmaf(dk[v], F[v], p);
+                }
+                pb[i] = p;
+                // this warp is done with the slot; the producer refills it for edge e + RING_DEPTH once
+                // every warp of the block has said so
+                __syncwarp();
+                if (lane == 0) ring_bar_arrive(ring.empty + slot);
+                if (producer && eb + i + RING_DEPTH < e1) {
+                    if (lane == 0) {
+                        ring_bar_wait(ring.empty + slot, use & 1u);
+                        ring_bulk_load(ring.rows + slot * (9 * C), GM + (size_t)j_ahead * (9 * C), ROW_BYTES,
+                                       ring.full + slot);
+                    }
+                    if (eb + i + 1 + RING_DEPTH < e1) j_ahead = __ldg(ejk + eb + i + 1 + RING_DEPTH).x;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16, h = 4; h >= 1; o >>= 1, h >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const float send = up ? pb[i] : pb[i + h];
+                const float keep = up ? pb[i + h] : pb[i];
+                pb[i] = keep + __shfl_xor_sync(NNP_FULL_MASK, send, o);
+            }
+        }
+        float tot = pb[0];
+        tot += __shfl_xor_sync(NNP_FULL_MASK, tot, 2);
+        tot += __shfl_xor_sync(NNP_FULL_MASK, tot, 1);
+        const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && eb + idx < e1 && __ldg(ejk + eb + idx).x != s) gd_slot[eb + idx] = tot;
+    }
+    float *out = GY + ((size_t)s * 9 + Q0) * C + cb;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+// launched with exactly 64 * NPARTS threads: one receiver per block
+template <int C, int CPL>
+__global__ void __launch_bounds__(64 * (C / (32 * CPL)), 8 / (C / (32 * CPL))) k_edge_message_bwd_ring(TnDev d, int layer, const float *GM,
+                                                                                  float *GY, float *gd_layer)
+{
+    constexpr int NPARTS = C / (32 * CPL);
+    __shared__ __align__(128) float rows[RING_DEPTH * 9 * C];
+    __shared__ uint64_t bars[2 * RING_DEPTH];
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s = blockIdx.x;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RING_DEPTH; ++i) {
+            ring_bar_init(bars + i, 1);                        // full: the producer's expect_tx arrival
+            ring_bar_init(bars + RING_DEPTH + i, 2 * NPARTS);  // empty: one arrival per warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int part = warp >> 1, half = warp & 1;
+    const int cb = part * 32 * CPL + lane * CPL;
+    const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
+    float *gd_slot = gd_layer + (size_t)(2 * part + half) * d.capacity;
+    RowRing<C> ring{rows, bars, bars + RING_DEPTH};
+    if (half == 0) message_bwd_row_ring<C, CPL, 0, 2, 0, 4>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb, ring, warp == 0);
+    else message_bwd_row_ring<C, CPL, 2, 1, 4, 5>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb, ring, false);
 }
 
 // Reverse of the edge op for the row of node a (the list is symmetric, so the scatter to senders
@@ -1283,7 +1630,7 @@ __global__ void __launch_bounds__(256) k_forces(TnDev d)
             vy += ue.y - ur.y;
             vz += ue.z - ur.z;
         }
-        for (int p = 0; p < d.nparts * (d.m.num_layers + 1); ++p) {
+        for (int p = 0; p < d.gd_slots * (d.m.num_layers + 1); ++p) {
             const size_t po = (size_t)p * d.capacity;
             gd += d.g_d[po + e] + d.g_d[po + er];
         }
@@ -1315,7 +1662,10 @@ size_t carve(TnDev &d, void *ws)
     d.newpos = ar.take<int>(cap);
     d.geoA = ar.take<float4>(cap);
     d.geoB = ar.take<float4>(cap);
-    d.g_d = ar.take<float>(cap * NNP_PARTS * (size_t)(L + 1));
+    d.ejk = ar.take<int2>(cap);
+    d.hwV = ar.take<float4>(cap);
+    d.hwD = ar.take<float4>(cap);
+    d.g_d = ar.take<float>(cap * NNP_GD_SLOTS * (size_t)(L + 1));
     d.g_u = ar.take<float4>(cap * NNP_PARTS);
     d.zs = ar.take<int>(n);
     d.sample_ptr = ar.take<int>((size_t)d.n_samples + 1);
@@ -1426,7 +1776,7 @@ GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n,
 // node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
 // through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
 struct EdgeTuning {
-    int emb, fwd, bwd, embbwd, bwd_block, fwd_block, emb_block;
+    int emb, fwd, bwd, embbwd, bwd_block, fwd_block, emb_block, bwd_split;
 };
 static int env_int(const char *name, int fallback)
 {
@@ -1437,7 +1787,9 @@ static const EdgeTuning &edge_tuning()
 {
     static const EdgeTuning t = {env_int("NNP_CPL_EMB", 4), env_int("NNP_CPL_FWD", 4),
                                  env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
-                                 std::min(env_int("NNP_BWD_BLOCK", 64), 128), env_int("NNP_FWD_BLOCK", 64), env_int("NNP_EMB_BLOCK", 128)};
+                                 std::min(env_int("NNP_BWD_BLOCK", 128), 128), std::min(env_int("NNP_FWD_BLOCK", 64), 128), env_int("NNP_EMB_BLOCK", 128),
+                                 env_int("NNP_BWD_SPLIT", 1)};   // 1 = register gather, two warps per receiver (default); 2 = bulk-copy ring
+                                                                // (measured slower: 2.15 vs 1.30 ms per step); 0 = one warp per part, monomial tables
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -1469,6 +1821,7 @@ int run_step(TnDev &d, cudaStream_t st)
             return C / (32 * cpl);
         };
         d.nparts = std::max(parts(tune.bwd), parts(tune.embbwd));
+        d.gd_slots = std::max(parts(tune.embbwd), (tune.bwd_split ? 2 : 1) * parts(tune.bwd));
     }
     int rc;
 #define RUN(x)            \
@@ -1548,7 +1901,9 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
         { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.nparts * d.capacity))); } 
+        if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd_ring<C, CPL><<<NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
         // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }
