@@ -56,6 +56,7 @@ __global__ void k_langevin_middle(double *__restrict__ pos, double *__restrict__
                                   double dt, double c1, double c2, float *__restrict__ pos32_out,
                                   int *__restrict__ flag, int n)
 {
+    NNP_PDL_SYNC();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double half_dt = 0.5 * dt;
@@ -113,6 +114,7 @@ __global__ void k_langevin_middle(double *__restrict__ pos, double *__restrict__
 
 __global__ void k_advance_counter(unsigned long long *counter)
 {
+    NNP_PDL_SYNC();
     counter[0] += 1ull;
 }
 
@@ -127,11 +129,11 @@ extern "C" int nnp_md_langevin_middle(double *pos, double *vel, const float *for
     NNP_CHECK_ARG(pos && vel && forces && acc_scale && sigma && n >= 1, "bad arguments to nnp_md_langevin_middle");
     NNP_CHECK_ARG(dt > 0.0 && c1 >= 0.0 && c1 <= 1.0 && c2 >= 0.0, "bad integrator coefficients");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    k_langevin_middle<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(
+    nnp_launch((k_langevin_middle), NNP_GRID(nnp_blocks(n, 256)), 256, 0, st, 
         pos, vel, forces, acc_scale, sigma, noise, (unsigned long long)seed,
         reinterpret_cast<const unsigned long long *>(step_counter), dt, c1, c2, pos32_out, nonfinite_flag, n);
     if (step_counter)
-        k_advance_counter<<<NNP_GRID(1), 1, 0, st>>>(reinterpret_cast<unsigned long long *>(step_counter));
+        nnp_launch((k_advance_counter), NNP_GRID(1), 1, 0, st, reinterpret_cast<unsigned long long *>(step_counter));
     NNP_CHECK_LAUNCH("langevin_middle");
     return NNP_OK;
 }

@@ -107,6 +107,7 @@ __device__ __forceinline__ double pair_delta(const Metric &m, double ax, double 
 __global__ void k_sample_ptr(const int *__restrict__ batch, int n, int n_samples,
                              int *__restrict__ sample_ptr, int *__restrict__ counts)
 {
+    NNP_PDL_SYNC();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < 4) counts[b] = 0;
     if (b > n_samples) return;
@@ -122,6 +123,7 @@ __global__ void k_sample_ptr(const int *__restrict__ batch, int n, int n_samples
 // ---- open-boundary grid: bounding box reduction (neighbors.py:116-124)
 __global__ void k_bounds_partial(const double *__restrict__ pos, int n, double *__restrict__ partial)
 {
+    NNP_PDL_SYNC();
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
 #pragma unroll
@@ -156,6 +158,7 @@ __global__ void k_bounds_partial(const double *__restrict__ pos, int n, double *
 
 __global__ void k_grid_setup(NlArgs a, int n_partial)
 {
+    NNP_PDL_SYNC();
     if (threadIdx.x != 0) return;
     GridDev g;
     if (a.periodic) {
@@ -221,6 +224,7 @@ __global__ void k_grid_setup(NlArgs a, int n_partial)
 
 __global__ void k_cell_assign(NlArgs a)
 {
+    NNP_PDL_SYNC();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     const GridDev g = *a.grid;
@@ -250,6 +254,7 @@ __global__ void k_cell_assign(NlArgs a)
 
 __global__ void k_cell_scatter(NlArgs a)
 {
+    NNP_PDL_SYNC();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     int c = a.cell_id[i];
@@ -261,6 +266,7 @@ __global__ void k_cell_scatter(NlArgs a)
 // np.argsort(flat, kind="stable") (neighbors.py:129) whatever order the atomics ran in.
 __global__ void k_cell_rank(NlArgs a)
 {
+    NNP_PDL_SYNC();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     int c = a.cell_id[i];
@@ -305,6 +311,7 @@ __global__ void k_cell_rank(NlArgs a)
 
 __global__ void k_identity_order(NlArgs a)
 {
+    NNP_PDL_SYNC();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     a.sidx[i] = i;
@@ -391,6 +398,7 @@ __device__ __forceinline__ bool prefilter(const NlArgs &a, double ax, double ay,
 template <bool FILL, typename OutT>
 __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
 {
+    NNP_PDL_SYNC();
     __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_queue[NL_WARPS][64];
@@ -641,6 +649,7 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
 template <typename OutT>
 __global__ void k_pad_tail(NlArgs a)
 {
+    NNP_PDL_SYNC();
     // fixed grid, element-wise over the three tails (the row count is only known on the device, so a
     // grid sized for the whole capacity would launch mostly idle blocks)
     const int total = a.row_ptr[a.n];
@@ -657,6 +666,7 @@ __global__ void k_pad_tail(NlArgs a)
 
 __global__ void k_f32_to_f64(const float *__restrict__ src, double *__restrict__ dst, int64_t n)
 {
+    NNP_PDL_SYNC();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = (double)src[i];
 }
@@ -665,6 +675,7 @@ __global__ void k_pullback(const int *__restrict__ pairs, const double *__restri
                            const double *__restrict__ dists, const double *__restrict__ g, int count,
                            double *__restrict__ grad, int *__restrict__ flag)
 {
+    NNP_PDL_SYNC();
     int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= count) return;
     int i = pairs[2 * e], j = pairs[2 * e + 1];
@@ -823,48 +834,48 @@ extern "C" int nnp_nl_build(const nnp_nl_params *p, const double *pos, const int
 
     const int n = a.n;
     const int nb = nnp_blocks(n, 256);
-    { NNP_PROF("k_sample_ptr", stream); k_sample_ptr<<<NNP_GRID(nnp_blocks(a.n_samples + 1, 256)), 256, 0, stream>>>(batch, n, a.n_samples, a.sample_ptr, counts); }
+    { NNP_PROF("k_sample_ptr", stream); nnp_launch((k_sample_ptr), NNP_GRID(nnp_blocks(a.n_samples + 1, 256)), 256, 0, stream, batch, n, a.n_samples, a.sample_ptr, counts); }
 
     if (a.strategy == NNP_STRATEGY_CELL) {
         int n_partial = 1;
         if (!a.periodic) {
             n_partial = std::min(BOUNDS_BLOCKS, nb);
-            { NNP_PROF("k_bounds_partial", stream); k_bounds_partial<<<NNP_GRID(n_partial), NL_THREADS, 0, stream>>>(pos, n, a.bounds_partial); }
+            { NNP_PROF("k_bounds_partial", stream); nnp_launch((k_bounds_partial), NNP_GRID(n_partial), NL_THREADS, 0, stream, pos, n, a.bounds_partial); }
         }
-        { NNP_PROF("k_grid_setup", stream); k_grid_setup<<<NNP_GRID(1), 32, 0, stream>>>(a, n_partial); }
+        { NNP_PROF("k_grid_setup", stream); nnp_launch((k_grid_setup), NNP_GRID(1), 32, 0, stream, a, n_partial); }
         // cell_start (max_cells + 1 ints) and cell_cursor (max_cells ints) are carved back to back
         cudaMemsetAsync(a.cell_start, 0, (size_t)((char *)(a.cell_cursor + a.max_cells) - (char *)a.cell_start), stream);
-        { NNP_PROF("k_cell_assign", stream); k_cell_assign<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
+        { NNP_PROF("k_cell_assign", stream); nnp_launch((k_cell_assign), NNP_GRID(nb), 256, 0, stream, a); }
         {
             NNP_PROF("scan_cells", stream);
             rc = nnp_exclusive_scan_i32(a.cell_start, a.cell_start, (int64_t)a.max_cells + 1,
                                         scan_temp, stream);
         }
         if (rc) return rc;
-        { NNP_PROF("k_cell_scatter", stream); k_cell_scatter<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
-        { NNP_PROF("k_cell_rank", stream); k_cell_rank<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
+        { NNP_PROF("k_cell_scatter", stream); nnp_launch((k_cell_scatter), NNP_GRID(nb), 256, 0, stream, a); }
+        { NNP_PROF("k_cell_rank", stream); nnp_launch((k_cell_rank), NNP_GRID(nb), 256, 0, stream, a); }
     } else {
-        { NNP_PROF("k_identity_order", stream); k_identity_order<<<NNP_GRID(nb), 256, 0, stream>>>(a); }
+        { NNP_PROF("k_identity_order", stream); nnp_launch((k_identity_order), NNP_GRID(nb), 256, 0, stream, a); }
     }
     NNP_CHECK_LAUNCH("neighbor binning");
 
     const int row_blocks = nnp_blocks(n, NL_WARPS);
     const bool f32 = p->flags & NNP_NL_F32_OUT;
-    { NNP_PROF("k_rows_count", stream); k_rows<false, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
+    { NNP_PROF("k_rows_count", stream); nnp_launch((k_rows<false, double>), NNP_GRID(row_blocks), NL_THREADS, 0, stream, a); }
     {
         NNP_PROF("scan_rows", stream);
         rc = nnp_exclusive_scan_i32(a.row_count, a.row_ptr, (int64_t)n + 1, scan_temp, stream);
     }
     if (rc) return rc;
     if (f32)
-        { NNP_PROF("k_rows_fill", stream); k_rows<true, float><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
+        { NNP_PROF("k_rows_fill", stream); nnp_launch((k_rows<true, float>), NNP_GRID(row_blocks), NL_THREADS, 0, stream, a); }
     else
-        { NNP_PROF("k_rows_fill", stream); k_rows<true, double><<<NNP_GRID(row_blocks), NL_THREADS, 0, stream>>>(a); }
+        { NNP_PROF("k_rows_fill", stream); nnp_launch((k_rows<true, double>), NNP_GRID(row_blocks), NL_THREADS, 0, stream, a); }
     if (!(p->flags & NNP_NL_NO_PAD)) {
         if (f32)
-            { NNP_PROF("k_pad_tail", stream); k_pad_tail<float><<<NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream>>>(a); }
+            { NNP_PROF("k_pad_tail", stream); nnp_launch((k_pad_tail<float>), NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream, a); }
         else
-            { NNP_PROF("k_pad_tail", stream); k_pad_tail<double><<<NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream>>>(a); }
+            { NNP_PROF("k_pad_tail", stream); nnp_launch((k_pad_tail<double>), NNP_GRID(std::min(nnp_blocks(a.capacity, 256), 148 * 8)), 256, 0, stream, a); }
     }
     NNP_CHECK_LAUNCH("neighbor rows");
     return NNP_OK;
@@ -874,7 +885,7 @@ extern "C" int nnp_f32_to_f64(const float *src, double *dst, int64_t n, nnp_stre
 {
     NNP_CHECK_ARG(src && dst && n >= 0, "bad arguments to nnp_f32_to_f64");
     if (n == 0) return NNP_OK;
-    k_f32_to_f64<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+    nnp_launch((k_f32_to_f64), NNP_GRID(nnp_blocks(n, 256)), 256, 0, static_cast<cudaStream_t>(stream), src, dst, n);
     NNP_CHECK_LAUNCH("f32_to_f64");
     return NNP_OK;
 }
@@ -892,7 +903,7 @@ extern "C" int nnp_distance_pullback(const int32_t *pairs, const double *deltas,
     cudaMemsetAsync(grad, 0, 3 * (size_t)n_atoms * sizeof(double), stream);
     cudaMemsetAsync(flag_out, 0x7f, sizeof(int), stream);  // 0x7f7f7f7f = none
     if (count > 0)
-        k_pullback<<<NNP_GRID(nnp_blocks(count, 256)), 256, 0, stream>>>(pairs, deltas, dists, g, count, grad,
+        nnp_launch((k_pullback), NNP_GRID(nnp_blocks(count, 256)), 256, 0, stream, pairs, deltas, dists, g, count, grad,
                                                               flag_out);
     NNP_CHECK_LAUNCH("distance_pullback");
     return NNP_OK;

@@ -36,6 +36,47 @@ extern thread_local int g_nnp_launch_count;
 // wraps the grid argument of every launch: counts kernels enqueued by this library
 #define NNP_GRID(x) (++g_nnp_launch_count, (x))
 
+// ---- programmatic dependent launch (PDL)
+// Every kernel of the library starts with NNP_PDL_SYNC(): wait until the grid it depends on has
+// completed (and its writes are visible), then allow the NEXT kernel of the stream to be scheduled.
+// With the launch attribute below the next kernel's blocks are placed as soon as the last wave of
+// this one has started, run whatever precedes their own NNP_PDL_SYNC() (barrier / tensor-memory
+// set-up, constant weights), and wait there: the launch latency and the ramp-up of a kernel overlap
+// the tail of its predecessor instead of following it (~60 kernel boundaries per step).  Anything read
+// before NNP_PDL_SYNC() must have been written at least two kernels earlier (or never in the step).
+// MEASURED (profiles/r2_summary.md): the captured step graph of config C replays in 5.01 ms with the
+// attribute against 4.50 ms without (the waiting blocks of the next kernel take SM slots from the
+// tail of the running one), 0.266 against 0.273 ms on the 22-atom config A.  The attribute is
+// therefore only set with NNP_PDL=1 in the environment; without it NNP_PDL_SYNC() is a no-op.
+#if defined(__CUDA_ARCH__)
+#define NNP_PDL_SYNC()                                            \
+    do {                                                          \
+        asm volatile("griddepcontrol.wait;" ::: "memory");        \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+#else
+#define NNP_PDL_SYNC() do { } while (0)
+#endif
+
+bool nnp_pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t nnp_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     cudaStream_t stream, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = nnp_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // When profiling is on (nnp_profile_begin), NNP_PROF scopes record a cudaEvent pair around the
 // launches they enclose; nnp_profile_report sums the elapsed time per label.
 void nnp_prof_mark(const char *label, cudaStream_t stream, int begin);

@@ -28,6 +28,7 @@ __global__ void k_prior_pairs(nnp_prior_params p, const int *__restrict__ pairs,
                               const double *__restrict__ rvdw, double *__restrict__ per_atom,
                               double *__restrict__ forces)
 {
+    NNP_PDL_SYNC();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int count = count_dev ? count_dev[0] : count_host;
     if (r >= count) return;
@@ -112,7 +113,7 @@ extern "C" int nnp_priors_pair_terms(const nnp_prior_params *p, const int32_t *p
     cudaMemsetAsync(per_atom, 0, sizeof(double) * (size_t)n_atoms, st);
     if (forces) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * (size_t)n_atoms, st);
     if (count_host > 0)
-        k_prior_pairs<<<NNP_GRID(nnp_blocks(count_host, 256)), 256, 0, st>>>(
+        nnp_launch((k_prior_pairs), NNP_GRID(nnp_blocks(count_host, 256)), 256, 0, st, 
             *p, pairs, deltas, dists, count_dev, count_host, full_list, charge, znum, zpow, c6, rvdw, per_atom,
             forces);
     NNP_CHECK_LAUNCH("prior_pairs");

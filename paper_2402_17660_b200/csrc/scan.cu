@@ -1,6 +1,7 @@
 // Exclusive prefix sum of int32 arrays: block-local scan, scan of block totals, add-back.
 // Used for cell starts (neighbors.py:127-133 does bincount + cumsum) and CSR row offsets.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include "nnp_common.cuh"
 
@@ -17,6 +18,16 @@ void nnp_set_error(const char *fmt, ...)
 extern "C" const char *nnp_last_error(void) { return g_last_error; }
 
 thread_local int g_nnp_launch_count = 0;
+
+bool nnp_pdl_enabled()
+{
+    static const bool on = [] {
+        const char *v = getenv("NNP_PDL");
+        return v && v[0] == '1';      // off unless asked for: measured slower inside the step graph
+    }();
+    return on;
+}
+
 extern "C" int nnp_launch_count(int reset)
 {
     int v = g_nnp_launch_count;
@@ -139,6 +150,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total)
 
 __global__ void scan_tiles(const int32_t *in, int32_t *out, int64_t n, int32_t *tile_totals)
 {
+    NNP_PDL_SYNC();
     const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     int v[SCAN_ITEMS];
     int sum = 0;
@@ -159,6 +171,7 @@ __global__ void scan_tiles(const int32_t *in, int32_t *out, int64_t n, int32_t *
 
 __global__ void scan_totals(int32_t *tile_totals, int nt)
 {
+    NNP_PDL_SYNC();
     __shared__ int carry_s;
     if (threadIdx.x == 0) carry_s = 0;
     __syncthreads();
@@ -177,6 +190,7 @@ __global__ void scan_totals(int32_t *tile_totals, int nt)
 
 __global__ void scan_add(int32_t *__restrict__ out, int64_t n, const int32_t *__restrict__ tile_totals)
 {
+    NNP_PDL_SYNC();
     const int add = tile_totals[blockIdx.x];
     const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
 #pragma unroll
@@ -193,10 +207,10 @@ int nnp_exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, int32_t *
 {
     if (n <= 0) return NNP_OK;
     const int nt = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
-    scan_tiles<<<NNP_GRID(nt), SCAN_THREADS, 0, stream>>>(in, out, n, temp);
+    nnp_launch((scan_tiles), NNP_GRID(nt), SCAN_THREADS, 0, stream, in, out, n, temp);
     if (nt > 1) {
-        scan_totals<<<NNP_GRID(1), SCAN_THREADS, 0, stream>>>(temp, nt);
-        scan_add<<<NNP_GRID(nt), SCAN_THREADS, 0, stream>>>(out, n, temp);
+        nnp_launch((scan_totals), NNP_GRID(1), SCAN_THREADS, 0, stream, temp, nt);
+        nnp_launch((scan_add), NNP_GRID(nt), SCAN_THREADS, 0, stream, out, n, temp);
     }
     NNP_CHECK_LAUNCH("exclusive_scan");
     return NNP_OK;

@@ -153,6 +153,7 @@ __device__ __forceinline__ void gemm_epilogue4(const GemmArgs &g, int r, int c, 
 template <int PRO, int EPI, bool MMA>
 __global__ void __launch_bounds__(GEMM_THREADS) gemm_nt_kernel(GemmBatch batch)
 {
+    NNP_PDL_SYNC();
     const GemmArgs &g = batch.g[blockIdx.z];
     const int m0 = blockIdx.x * GEMM_BM;
     const int n0 = blockIdx.y * GEMM_BN;

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(THREADS) gemm_nt_tc5_kernel(GemmBatch batch)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_d = tmem_base_s;
+    NNP_PDL_SYNC();   // barrier and tensor-memory set-up above overlap the previous kernel's tail
 
     // loader mapping: 8 threads per row (one 16-byte chunk each), 16 rows per pass
     const int lrow = tid >> 3, lchunk = tid & 7;
@@ -440,6 +441,10 @@ __global__ void __launch_bounds__(ST_THREADS, 1) gemm_stream_kernel(GemmBatch ba
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(&w_bar);        // only the MMA thread waits for the weights; loads start at once
     }
+    // Everything above reads only the weights, which no kernel of the step writes less than two
+    // launches before a GEMM that uses them, so it runs while the previous kernel drains; the
+    // activations may only be touched from here on.
+    NNP_PDL_SYNC();
 
     if (warp >= 5 && warp < 13) {
         // ============================================================ producers (256 threads)
@@ -657,7 +662,7 @@ static int launch_stream(const GemmBatch &b, int count, cudaStream_t stream)
         used += c;
     }
     for (int i = count; i < 4; ++i) sc.cta_begin[i] = used;
-    gemm_stream_kernel<PRO, EPI><<<NNP_GRID(used), ST_THREADS, smem, stream>>>(b, sc);
+    nnp_launch((gemm_stream_kernel<PRO, EPI>), NNP_GRID(used), ST_THREADS, smem, stream, b, sc);
     NNP_CHECK_LAUNCH("gemm_stream");
     return NNP_OK;
 }
@@ -671,7 +676,7 @@ static int launch_nt(const GemmBatch &b, int count, int maxM, int maxN, cudaStre
         cudaFuncSetAttribute(gemm_nt_tc5_kernel<PRO, EPI, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     dim3 grid(NNP_GRID((maxM + BM - 1) / BM), (maxN + NT - 1) / NT, count);
-    gemm_nt_tc5_kernel<PRO, EPI, NT><<<grid, THREADS, smem, stream>>>(b);
+    nnp_launch((gemm_nt_tc5_kernel<PRO, EPI, NT>), grid, THREADS, smem, stream, b);
     NNP_CHECK_LAUNCH("gemm_nt_tc5");
     return NNP_OK;
 }
@@ -727,9 +732,9 @@ static int gemm_launch(const GemmBatch &b, int count, cudaStream_t stream)
     }
     dim3 grid(NNP_GRID((maxM + GEMM_BM - 1) / GEMM_BM), (maxN + GEMM_BN - 1) / GEMM_BN, count);
     if (t_nnp_gemm_mode)
-        gemm_nt_kernel<PRO, EPI, true><<<grid, GEMM_THREADS, 0, stream>>>(b);
+        nnp_launch((gemm_nt_kernel<PRO, EPI, true>), grid, GEMM_THREADS, 0, stream, b);
     else
-        gemm_nt_kernel<PRO, EPI, false><<<grid, GEMM_THREADS, 0, stream>>>(b);
+        nnp_launch((gemm_nt_kernel<PRO, EPI, false>), grid, GEMM_THREADS, 0, stream, b);
     NNP_CHECK_LAUNCH("gemm_nt");
     return NNP_OK;
 }

@@ -121,6 +121,7 @@ __device__ __forceinline__ bool overflowed(const TnDev &d)
 // ------------------------------------------------------------------------------- setup
 __global__ void k_prep_nodes(TnDev d)
 {
+    NNP_PDL_SYNC();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (d.present)
         for (int z = s; z < d.m.max_z; z += gridDim.x * blockDim.x) d.present[z] = 0;
@@ -153,6 +154,7 @@ __device__ __forceinline__ int knot_of(float tx, int num_knots, float &t)
 // cosine cutoff as radial.py:11-39, u as radial.py:57.
 __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
 {
+    NNP_PDL_SYNC();
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
 // sender's row of the caller's list (sorted by sender), mapped through newpos.
 __global__ void k_edge_rev(TnDev d)
 {
+    NNP_PDL_SYNC();
     if (overflowed(d)) return;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= d.row_ptr[d.n]) return;
@@ -285,6 +288,7 @@ __device__ __forceinline__ int group_of(int q) { return q == 0 ? 0 : (q < 4 ? 1 
 // dE/dX0 over channels for every (species, radial basis function).
 __global__ void __launch_bounds__(256) k_embed_slots(TnDev d)
 {
+    NNP_PDL_SYNC();
     __shared__ int sp[EMB_SLOTS];
     const int C = d.m.channels;
     if (threadIdx.x < 32) {
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(256) k_embed_slots(TnDev d)
 template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(256) k_embed_edge(TnDev d)
 template <int C>
 __global__ void __launch_bounds__(256) k_embed_ln(TnDev d)
 {
+    NNP_PDL_SYNC();
     constexpr int CPL = C / 32;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -421,6 +427,7 @@ __device__ __forceinline__ void st9(float *base, int C, const float *c9)
 __global__ void k_normalize(const float *__restrict__ X, const float *__restrict__ e1,
                             float *__restrict__ Xh, float *__restrict__ nx, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -443,6 +450,7 @@ __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict
                            float *__restrict__ Xn, float *__restrict__ Xh_next,
                            float *__restrict__ nx_next, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -463,6 +471,7 @@ __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict
 __global__ void k_residual_bwd(const float *__restrict__ G, const float *__restrict__ Dc,
                                float *__restrict__ GD, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -478,6 +487,7 @@ __global__ void k_node_product_bwd(const float *__restrict__ Mc, const float *__
                                    const float *__restrict__ GQ, float *__restrict__ GM,
                                    float *__restrict__ GY, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -496,6 +506,7 @@ __global__ void k_normalize_bwd(const float *__restrict__ GXa, const float *__re
                                 const float *__restrict__ Xh, const float *__restrict__ nx,
                                 float *__restrict__ GX, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -515,6 +526,7 @@ __global__ void k_embed_gate_bwd(const float *__restrict__ GX, const float *__re
                                  const float *__restrict__ e1, float *__restrict__ GXm,
                                  float *__restrict__ g_e1, int n, int C)
 {
+    NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * C) return;
     const int node = idx / C, c = idx - node * C;
@@ -627,6 +639,7 @@ __device__ __forceinline__ void message_row_part(const TnDev &d, const float *__
 template <int C, int CPL>
 __global__ void __launch_bounds__(128, 5) k_edge_message_split(TnDev d, int layer)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
@@ -788,6 +801,7 @@ template <int C, int CPL>
 __global__ void __launch_bounds__(128, 4) k_edge_message_bwd_split(TnDev d, int layer, const float *GM,
                                                                 float *GY, float *gd_layer)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
@@ -990,6 +1004,7 @@ template <int C, int CPL>
 __global__ void __launch_bounds__(64 * (C / (32 * CPL)), 8 / (C / (32 * CPL))) k_edge_message_bwd_ring(TnDev d, int layer, const float *GM,
                                                                                   float *GY, float *gd_layer)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     __shared__ __align__(128) float rows[RING_DEPTH * 9 * C];
     __shared__ uint64_t bars[2 * RING_DEPTH];
@@ -1026,6 +1041,7 @@ template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, const float *GM,
                                                           float *GY, float *gd_layer)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
@@ -1152,6 +1168,7 @@ __global__ void __launch_bounds__(256) k_edge_message_bwd(TnDev d, int layer, co
 template <int C>
 __global__ void __launch_bounds__(256) k_readout_feats(TnDev d, const float *X)
 {
+    NNP_PDL_SYNC();
     constexpr int CPL = C / 32;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1196,6 +1213,7 @@ __global__ void __launch_bounds__(256) k_readout_feats(TnDev d, const float *X)
 // also the head's own reverse (g_r1) and the caller's per-atom copy
 __global__ void k_head(TnDev d, int H)
 {
+    NNP_PDL_SYNC();
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (s >= d.n) return;
@@ -1218,6 +1236,7 @@ __global__ void k_head(TnDev d, int H)
 // per-sample sums in float64, fixed order (graphnet.py:411 segment_sum over batch)
 __global__ void __launch_bounds__(1024) k_energy_sum(TnDev d)
 {
+    NNP_PDL_SYNC();
     const int b = blockIdx.x;
     const int p0 = d.sample_ptr[b], p1 = d.sample_ptr[b + 1];
     double acc = 0.0;
@@ -1237,6 +1256,7 @@ __global__ void __launch_bounds__(1024) k_energy_sum(TnDev d)
 template <int C>
 __global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, float *GX)
 {
+    NNP_PDL_SYNC();
     constexpr int CPL = C / 32;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1302,6 +1322,7 @@ __global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, fl
 template <int C>
 __global__ void __launch_bounds__(256) k_embed_norm_bwd(TnDev d, float *GX0)
 {
+    NNP_PDL_SYNC();
     constexpr int CPL = C / 32;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1399,6 +1420,7 @@ __global__ void __launch_bounds__(256) k_embed_norm_bwd(TnDev d, float *GX0)
 template <int C, int CPL>
 __global__ void __launch_bounds__(256) k_embed_edge_bwd(TnDev d, const float *GX0)
 {
+    NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
     if (overflowed(d)) return;
     if (d.embed_fast && d.embed_fast[0]) return;   // the projected kernels do this step's embedding reverse
@@ -1519,6 +1541,7 @@ constexpr int EMB_PROJ_STRIDE = 9 * EMB_K + 4;   // slot stride: slots land on d
 __global__ void __launch_bounds__(EMB_PROJ_WARPS * 32) k_embed_edge_bwd_proj(TnDev d, const float *Hs,
                                                                              const float *Hr)
 {
+    NNP_PDL_SYNC();
     __shared__ __align__(16) float hc_all[EMB_PROJ_WARPS][EMB_SLOTS * EMB_PROJ_STRIDE];
     __shared__ __align__(16) float hb_all[EMB_PROJ_WARPS][EMB_SLOTS * 9 + 4];
     __shared__ __align__(16) float mu_s[EMB_K], beta_s[EMB_K];
@@ -1610,6 +1633,7 @@ __global__ void __launch_bounds__(EMB_PROJ_WARPS * 32) k_embed_edge_bwd_proj(TnD
 // fixed-order butterfly sums the three components, so the result is reproducible.
 __global__ void __launch_bounds__(256) k_forces(TnDev d)
 {
+    NNP_PDL_SYNC();
     if (overflowed(d)) return;
     const int lane = threadIdx.x & 31;
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1830,14 +1854,14 @@ int run_step(TnDev &d, cudaStream_t st)
         if (rc) return rc; \
     } while (0)
 
-    { NNP_PROF("k_prep_nodes", st); k_prep_nodes<<<NNP_GRID(nnp_blocks(n, 256)), 256, 0, st>>>(d); }
-    { NNP_PROF("k_edge_order", st); k_edge_order<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
-    { NNP_PROF("k_edge_rev", st); k_edge_rev<<<NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st>>>(d); }
-    if (d.m.embed_projection && d.forces) { NNP_PROF("k_embed_slots", st); k_embed_slots<<<NNP_GRID(3 * 2 * EMB_SLOTS), 256, 0, st>>>(d); }
+    { NNP_PROF("k_prep_nodes", st); nnp_launch((k_prep_nodes), NNP_GRID(nnp_blocks(n, 256)), 256, 0, st, d); }
+    { NNP_PROF("k_edge_order", st); nnp_launch((k_edge_order), NNP_GRID(warp_blocks), 256, 0, st, d); }
+    { NNP_PROF("k_edge_rev", st); nnp_launch((k_edge_rev), NNP_GRID(nnp_blocks(d.capacity, 256)), 256, 0, st, d); }
+    if (d.m.embed_projection && d.forces) { NNP_PROF("k_embed_slots", st); nnp_launch((k_embed_slots), NNP_GRID(3 * 2 * EMB_SLOTS), 256, 0, st, d); }
 
     // ---- embedding
-    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (k_embed_edge<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d))); }
-    { NNP_PROF("k_embed_ln", st); k_embed_ln<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
+    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d))); }
+    { NNP_PROF("k_embed_ln", st); nnp_launch((k_embed_ln<C>), NNP_GRID(warp_blocks), 256, 0, st, d); }
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.ln0, m.es0_w, m.es0_b, d.e0, n, 2 * C, C);
@@ -1857,18 +1881,18 @@ int run_step(TnDev &d, cudaStream_t st)
 
     // ---- interaction layers
     for (int l = 0; l < L; ++l) {
-        if (l == 0) { NNP_PROF("k_normalize", st); k_normalize<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xm, d.e1, d.Xh[l], d.nx[l], n, C); }
+        if (l == 0) { NNP_PROF("k_normalize", st); nnp_launch((k_normalize), NNP_GRID(ew_blocks), 256, 0, st, d.Xm, d.e1, d.Xh[l], d.nx[l], n, C); }
         GemmBatch my = mix_gemm(d.Xh[l], m.layer_t_w[l], d.Yc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(my, 3, st))); }
-        { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (k_edge_message_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st>>>(d, l))); }
+        { NNP_PROF("k_edge_message", st); EDGE_DISPATCH(C, tune.fwd, (nnp_launch((k_edge_message_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.fwd_block / 32)), tune.fwd_block, 0, st, d, l))); }
         GemmBatch md = mix_gemm(d.Qc, m.layer_t_w[l] + 3, d.Dc[l], n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(md, 3, st))); }
-        { NNP_PROF("k_residual", st); k_residual<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Xh[l], d.Dc[l], Xother, l + 1 < L ? d.Xh[l + 1] : nullptr, l + 1 < L ? d.nx[l + 1] : nullptr, n, C); }
+        { NNP_PROF("k_residual", st); nnp_launch((k_residual), NNP_GRID(ew_blocks), 256, 0, st, d.Xh[l], d.Dc[l], Xother, l + 1 < L ? d.Xh[l + 1] : nullptr, l + 1 < L ? d.nx[l + 1] : nullptr, n, C); }
         std::swap(X, Xother);
     }
 
     // ---- readout
-    { NNP_PROF("k_readout_feats", st); k_readout_feats<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, X); }
+    { NNP_PROF("k_readout_feats", st); nnp_launch((k_readout_feats<C>), NNP_GRID(warp_blocks), 256, 0, st, d, X); }
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.lnr, m.lin_w, m.lin_b, d.r0, n, C, 3 * C);
@@ -1877,8 +1901,8 @@ int run_step(TnDev &d, cudaStream_t st)
         b.g[0] = plain_gemm(d.sr0, m.h1_w, m.h1_b, d.r1, n, H, C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
     }
-    { NNP_PROF("k_head", st); k_head<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, H); }
-    { NNP_PROF("k_energy_sum", st); k_energy_sum<<<NNP_GRID(d.n_samples), (n / d.n_samples >= 2048 ? 1024 : 256), 0, st>>>(d); }
+    { NNP_PROF("k_head", st); nnp_launch((k_head), NNP_GRID(warp_blocks), 256, 0, st, d, H); }
+    { NNP_PROF("k_energy_sum", st); nnp_launch((k_energy_sum), NNP_GRID(d.n_samples), (n / d.n_samples >= 2048 ? 1024 : 256), 0, st, d); }
     NNP_CHECK_LAUNCH("tensornet forward");
     if (!d.forces) return NNP_OK;
 
@@ -1892,27 +1916,27 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
     }
     float *GX = d.G1, *Ga = d.G2, *Gb = d.G3;
-    { NNP_PROF("k_readout_bwd", st); k_readout_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, X, GX); }
+    { NNP_PROF("k_readout_bwd", st); nnp_launch((k_readout_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, X, GX); }
 
     for (int l = L - 1; l >= 0; --l) {
         // GX = dL/dX_{l+1}.  dL/dXh starts as GX itself.
-        { NNP_PROF("k_residual_bwd", st); k_residual_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Dc[l], Ga, n, C); }  // Ga = G_D
+        { NNP_PROF("k_residual_bwd", st); nnp_launch((k_residual_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, d.Dc[l], Ga, n, C); }  // Ga = G_D
         GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + 3, Gb, n, C);     // Gb = G_Q
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
-        { NNP_PROF("k_node_product_bwd", st); k_node_product_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
+        { NNP_PROF("k_node_product_bwd", st); nnp_launch((k_node_product_bwd), NNP_GRID(ew_blocks), 256, 0, st, d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
         // now Ga = G_M, Qc = G_Y (local part)
-        if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd_ring<C, CPL><<<NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd_split<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (k_edge_message_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st>>>(d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_ring<C, CPL>), NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
         // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
         GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }
-        { NNP_PROF("k_normalize_bwd", st); k_normalize_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, Ga, d.Xh[l], d.nx[l], Gb, n, C); }
+        { NNP_PROF("k_normalize_bwd", st); nnp_launch((k_normalize_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, Ga, d.Xh[l], d.nx[l], Gb, n, C); }
         std::swap(GX, Gb);
     }
 
     // ---- embedding reverse: X = Xm * gate
-    { NNP_PROF("k_embed_gate_bwd", st); k_embed_gate_bwd<<<NNP_GRID(ew_blocks), 256, 0, st>>>(GX, d.Xm, d.e1, Ga, d.g_e1, n, C); }  // Ga = G_Xm
+    { NNP_PROF("k_embed_gate_bwd", st); nnp_launch((k_embed_gate_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, d.Xm, d.e1, Ga, d.g_e1, n, C); }  // Ga = G_Xm
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.g_e1, m.es1_wT, nullptr, d.g_e0, n, 2 * C, 3 * C, d.e0, 2 * C);
@@ -1922,7 +1946,7 @@ int run_step(TnDev &d, cudaStream_t st)
         GemmBatch mx = mix_gemm(Ga, m.et_wT, Gb, n, C);                                 // Gb = G_X0 part
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
-    { NNP_PROF("k_embed_norm_bwd", st); k_embed_norm_bwd<C><<<NNP_GRID(warp_blocks), 256, 0, st>>>(d, Gb); }
+    { NNP_PROF("k_embed_norm_bwd", st); nnp_launch((k_embed_norm_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, Gb); }
     if (d.m.embed_projection) {
         // Hs = G_X0 against the sender-species weights, Hr against the receiver-species weights
         // (Ga and GX are free by now); then one lane per edge
@@ -1938,10 +1962,10 @@ int run_step(TnDev &d, cudaStream_t st)
         }
         { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(ms, 3, st))); }
         { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mr, 3, st))); }
-        { NNP_PROF("k_embed_edge_bwd_proj", st); k_embed_edge_bwd_proj<<<NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st>>>(d, Ga, GX); }
+        { NNP_PROF("k_embed_edge_bwd_proj", st); nnp_launch((k_embed_edge_bwd_proj), NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st, d, Ga, GX); }
     }
-    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (k_embed_edge_bwd<C, CPL><<<NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st>>>(d, Gb))); }
-    { NNP_PROF("k_forces", st); k_forces<<<NNP_GRID(warp_blocks), 256, 0, st>>>(d); }
+    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (nnp_launch((k_embed_edge_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d, Gb))); }
+    { NNP_PROF("k_forces", st); nnp_launch((k_forces), NNP_GRID(warp_blocks), 256, 0, st, d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
     return NNP_OK;
