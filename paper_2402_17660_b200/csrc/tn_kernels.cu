@@ -468,21 +468,6 @@ __global__ void k_residual(const float *__restrict__ Xh, const float *__restrict
     }
 }
 
-__global__ void k_residual_bwd(const float *__restrict__ G, const float *__restrict__ Dc,
-                               float *__restrict__ GD, int n, int C)
-{
-    NNP_PDL_SYNC();
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n * C) return;
-    const int node = idx / C, c = idx - node * C;
-    const size_t off = (size_t)node * 9 * C + c;
-    float g[9], dc[9], gd[9];
-    ld9(G + off, C, g);
-    ld9(Dc + off, C, dc);
-    residual_bwd(g, dc, gd);
-    st9(GD + off, C, gd);
-}
-
 __global__ void k_node_product_bwd(const float *__restrict__ Mc, const float *__restrict__ Yc,
                                    const float *__restrict__ GQ, float *__restrict__ GM,
                                    float *__restrict__ GY, int n, int C)
@@ -501,10 +486,18 @@ __global__ void k_node_product_bwd(const float *__restrict__ Mc, const float *__
     st9(GY + off, C, gy);
 }
 
-// dL/dXh arrives in two parts (the residual path GXa and the mixed-back edge path GXb)
-__global__ void k_normalize_bwd(const float *__restrict__ GXa, const float *__restrict__ GXb,
+// dL/dXh arrives in two parts (the residual path GXa and the mixed-back edge path GXb).  What
+// consumes dL/dX next is fused in, so the gradient makes one trip through HBM instead of two:
+//   * Dc_prev != NULL (layer l >= 1): also G_D = GX + GX*D^T + D^T*GX of layer l - 1 (k_residual_bwd);
+//   * Xm != NULL (layer 0): X = Xm * silu(e1)[grp] (k_embed_gate_bwd): G_Xm = GX * gate and
+//     g_e1 = <GX, Xm>_grp * silu'(e1) are written INSTEAD of GX, which nothing else reads.
+__global__ void k_normalize_bwd(const float *GXa, const float *__restrict__ GXb,
                                 const float *__restrict__ Xh, const float *__restrict__ nx,
-                                float *__restrict__ GX, int n, int C)
+                                float *GX /* may alias GXa: every thread reads its own nine values first */,
+                                const float *__restrict__ Dc_prev,
+                                float *__restrict__ GD, const float *__restrict__ Xm,
+                                const float *__restrict__ e1, float *__restrict__ GXm,
+                                float *__restrict__ g_e1, int n, int C)
 {
     NNP_PDL_SYNC();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -518,7 +511,27 @@ __global__ void k_normalize_bwd(const float *__restrict__ GXa, const float *__re
     for (int q = 0; q < 9; ++q) g[q] += g2[q];
     ld9(Xh + off, C, xh);
     normalize_bwd(g, xh, nx[idx], gx);
+    if (Xm) {
+        float xm[9], gxm[9];
+        ld9(Xm + off, C, xm);
+        const float *e = e1 + (size_t)node * 3 * C + 3 * c;
+        const float gate[3] = {nnp_silu(e[0]), nnp_silu(e[1]), nnp_silu(e[2])};
+#pragma unroll
+        for (int q = 0; q < 9; ++q) gxm[q] = gx[q] * gate[group_of(q)];
+        st9(GXm + off, C, gxm);
+        float *ge = g_e1 + (size_t)node * 3 * C + 3 * c;
+        ge[0] = c9_dot_I(gx, xm) * nnp_silu_grad(e[0]);
+        ge[1] = c9_dot_A(gx, xm) * nnp_silu_grad(e[1]);
+        ge[2] = c9_dot_S(gx, xm) * nnp_silu_grad(e[2]);
+        return;
+    }
     st9(GX + off, C, gx);
+    if (Dc_prev) {
+        float dc[9], gd[9];
+        ld9(Dc_prev + off, C, dc);
+        residual_bwd(gx, dc, gd);
+        st9(GD + off, C, gd);
+    }
 }
 
 // X = Xm * gate[grp], gate = silu(e1):  G_Xm = GX*gate ; g_e1 = <GX, Xm>_grp * silu'(e1)
@@ -1254,7 +1267,8 @@ __global__ void __launch_bounds__(1024) k_energy_sum(TnDev d)
 
 // reverse of k_readout_feats: GX = 2 * g_feats[grp] * X_part
 template <int C>
-__global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, float *GX)
+__global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, float *GX, const float *Dc_last,
+                                                     float *GD)
 {
     NNP_PDL_SYNC();
     constexpr int CPL = C / 32;
@@ -1308,14 +1322,34 @@ __global__ void __launch_bounds__(256) k_readout_bwd(TnDev d, const float *X, fl
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
         const int k = group_of(q);
-        float o[CPL];
 #pragma unroll
         for (int v = 0; v < CPL; ++v) {
             const float gf = rstd * (gxh[k][v] - s1 - xh[k][v] * s2);
-            o[v] = 2.0f * gf * x[q][v];
+            x[q][v] = 2.0f * gf * x[q][v];          // x now holds GX
         }
-        stv<CPL>(out + q * C, o);
+        stv<CPL>(out + q * C, x[q]);
     }
+    if (!Dc_last) return;
+    // fused k_residual_bwd of the last layer: G_D = GX + GX*D^T + D^T*GX
+    const float *pd = Dc_last + (size_t)s * 9 * C + cb;
+    float *og = GD + (size_t)s * 9 * C + cb;
+    float dcv[9][CPL];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ldv<CPL>(pd + q * C, dcv[q]);
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float g9[9], d9[9], gd9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            g9[q] = x[q][v];
+            d9[q] = dcv[q][v];
+        }
+        residual_bwd(g9, d9, gd9);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) dcv[q][v] = gd9[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) stv<CPL>(og + q * C, dcv[q]);
 }
 
 // G_X0 = G_X0part + 2 * g_n0 * X0, g_n0 = LayerNorm_C backward of g_ln0
@@ -1915,56 +1949,59 @@ int run_step(TnDev &d, cudaStream_t st)
         b.g[0] = plain_gemm(d.g_r0, m.lin_wT, nullptr, d.g_lnr, n, 3 * C, C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
     }
-    float *GX = d.G1, *Ga = d.G2, *Gb = d.G3;
-    { NNP_PROF("k_readout_bwd", st); nnp_launch((k_readout_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, X, GX); }
+    // Three gradient buffers: GX = dL/dX of the layer above (kept until the normalisation's reverse,
+    // which overwrites it in place), GB = G_D -> G_M -> next G_D (or G_Xm), GC = G_Q -> mixed-back G_Y.
+    float *GX = d.G1, *GB = d.G2, *GC = d.G3;
+    // GB = G_D of the last layer comes out of the readout's reverse (fused k_residual_bwd)
+    { NNP_PROF("k_readout_bwd", st); nnp_launch((k_readout_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, X, GX, L > 0 ? d.Dc[L - 1] : nullptr, GB); }
 
     for (int l = L - 1; l >= 0; --l) {
-        // GX = dL/dX_{l+1}.  dL/dXh starts as GX itself.
-        { NNP_PROF("k_residual_bwd", st); nnp_launch((k_residual_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, d.Dc[l], Ga, n, C); }  // Ga = G_D
-        GemmBatch mq = mix_gemm(Ga, m.layer_t_wT[l] + 3, Gb, n, C);     // Gb = G_Q
+        GemmBatch mq = mix_gemm(GB, m.layer_t_wT[l] + 3, GC, n, C);     // GC = G_Q
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mq, 3, st))); }
-        { NNP_PROF("k_node_product_bwd", st); nnp_launch((k_node_product_bwd), NNP_GRID(ew_blocks), 256, 0, st, d.Mc[l], d.Yc[l], Gb, Ga, d.Qc, n, C); }
-        // now Ga = G_M, Qc = G_Y (local part)
-        if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_ring<C, CPL>), NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, Ga, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse
-        GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], Ga, n, C);
+        { NNP_PROF("k_node_product_bwd", st); nnp_launch((k_node_product_bwd), NNP_GRID(ew_blocks), 256, 0, st, d.Mc[l], d.Yc[l], GC, GB, d.Qc, n, C); }
+        // now GB = G_M, Qc = G_Y (local part)
+        if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_ring<C, CPL>), NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse, which also writes
+        // what the next stage reads - G_D of layer l - 1, or the embedding gate's reverse at layer 0
+        GemmBatch mh = mix_gemm(d.Qc, m.layer_t_wT[l], GC, n, C);
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mh, 3, st))); }
-        { NNP_PROF("k_normalize_bwd", st); nnp_launch((k_normalize_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, Ga, d.Xh[l], d.nx[l], Gb, n, C); }
-        std::swap(GX, Gb);
+        if (l > 0) { NNP_PROF("k_normalize_bwd", st); nnp_launch((k_normalize_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, GC, d.Xh[l], d.nx[l], GX, d.Dc[l - 1], GB, nullptr, nullptr, nullptr, nullptr, n, C); }
+        else { NNP_PROF("k_normalize_bwd", st); nnp_launch((k_normalize_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, GC, d.Xh[l], d.nx[l], nullptr, nullptr, nullptr, d.Xm, d.e1, GB, d.g_e1, n, C); }
     }
+    // no interaction layer: X = Xm * gate went straight into the readout
+    if (L == 0) { NNP_PROF("k_embed_gate_bwd", st); nnp_launch((k_embed_gate_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, d.Xm, d.e1, GB, d.g_e1, n, C); }
 
-    // ---- embedding reverse: X = Xm * gate
-    { NNP_PROF("k_embed_gate_bwd", st); nnp_launch((k_embed_gate_bwd), NNP_GRID(ew_blocks), 256, 0, st, GX, d.Xm, d.e1, Ga, d.g_e1, n, C); }  // Ga = G_Xm
+    // ---- embedding reverse: GB = G_Xm
     {
         GemmBatch b{};
         b.g[0] = plain_gemm(d.g_e1, m.es1_wT, nullptr, d.g_e0, n, 2 * C, 3 * C, d.e0, 2 * C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_MUL_SILU_GRAD>(b, 1, st))); }
         b.g[0] = plain_gemm(d.g_e0, m.es0_wT, nullptr, d.g_ln0, n, C, 2 * C);
         { NNP_PROF("gemm_dense", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(b, 1, st))); }
-        GemmBatch mx = mix_gemm(Ga, m.et_wT, Gb, n, C);                                 // Gb = G_X0 part
+        GemmBatch mx = mix_gemm(GB, m.et_wT, GC, n, C);                                 // GC = G_X0 part
         { NNP_PROF("gemm_mix", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mx, 3, st))); }
     }
-    { NNP_PROF("k_embed_norm_bwd", st); nnp_launch((k_embed_norm_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, Gb); }
+    { NNP_PROF("k_embed_norm_bwd", st); nnp_launch((k_embed_norm_bwd<C>), NNP_GRID(warp_blocks), 256, 0, st, d, GC); }
     if (d.m.embed_projection) {
         // Hs = G_X0 against the sender-species weights, Hr against the receiver-species weights
-        // (Ga and GX are free by now); then one lane per edge
+        // (GB and GX are free by now); then one lane per edge
         nnp_gemm_weight ws[3], wr[3];
         for (int k = 0; k < 3; ++k) {
             ws[k].w = d.Wproj + (size_t)(k * 2 + 0) * EMB_SLOTS * EMB_K * C;
             wr[k].w = d.Wproj + (size_t)(k * 2 + 1) * EMB_SLOTS * EMB_K * C;
         }
-        GemmBatch ms = mix_gemm(Gb, ws, Ga, n, C), mr = mix_gemm(Gb, wr, GX, n, C);
+        GemmBatch ms = mix_gemm(GC, ws, GB, n, C), mr = mix_gemm(GC, wr, GX, n, C);
         for (int k = 0; k < 3; ++k) {
             ms.g[k].N = mr.g[k].N = EMB_SLOTS * EMB_K;
             ms.g[k].ldo = mr.g[k].ldo = EMB_SLOTS * EMB_K;
         }
         { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(ms, 3, st))); }
         { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mr, 3, st))); }
-        { NNP_PROF("k_embed_edge_bwd_proj", st); nnp_launch((k_embed_edge_bwd_proj), NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st, d, Ga, GX); }
+        { NNP_PROF("k_embed_edge_bwd_proj", st); nnp_launch((k_embed_edge_bwd_proj), NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st, d, GB, GX); }
     }
-    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (nnp_launch((k_embed_edge_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d, Gb))); }
+    { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (nnp_launch((k_embed_edge_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d, GC))); }
     { NNP_PROF("k_forces", st); nnp_launch((k_forces), NNP_GRID(warp_blocks), 256, 0, st, d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
 #undef RUN
