@@ -19,7 +19,7 @@ HEADERS = ("nnp_common.cuh", "tn_math.cuh", "tn_gemm.cuh", "tn_gemm_tc5.cuh", os
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-]
+] + [f"-D{d}" for d in os.environ.get("NNP_BUILD_DEFINES", "").split() if d]
 
 
 def find_nvcc() -> str:
