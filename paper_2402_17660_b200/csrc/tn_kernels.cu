@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(128, 5) k_edge_message_split(TnDev d, int laye
 // coefficient is loaded per edge.  The per-edge sum over channels is collected eight edges at a time:
 // every lane keeps its partial of eight edges and one transposing butterfly (7 + 2 shuffles) leaves
 // the eight totals in lanes 0, 4, ..., 28, which store them side by side.
-template <int C, int CPL, int K0, int NG, int Q0, int NQ, bool PIPE>
+template <int C, int CPL, int K0, int NG, int Q0, int NQ>
 __device__ __forceinline__ void message_bwd_row_part(const TnDev &d, const float *__restrict__ tab,
                                                      const float *__restrict__ GM, float *__restrict__ GY,
                                                      const float *__restrict__ Yown, float *__restrict__ gd_slot,
@@ -748,18 +748,10 @@ __device__ __forceinline__ void message_bwd_row_part(const TnDev &d, const float
     const float4 *__restrict__ hwV = d.hwV;
     const float4 *__restrict__ hwD = d.hwD;
     const float *gbase = GM + Q0 * C + cb;
-    // PIPE: the gather of edge e + 1 is requested after the knot loads of edge e and before edge e is
-    // evaluated, so that it overlaps the arithmetic (requested BEFORE the knot loads it was measured
-    // slower, 2.27 vs 1.31 ms per step: loads complete in issue order, so the knots waited for the row)
+    // MEASURED and dropped (profiles/r2_summary.md): keeping the gather of edge e + 1 in flight while
+    // edge e is evaluated (second row buffer, 147 registers) - 1.68 ms per step against 1.31 ms; the same
+    // with the gather requested before the knot loads 2.27 ms (loads complete in issue order).
     int2 jk = e0 < e1 ? __ldg(ejk + e0) : make_int2(0, 0);
-    float gn[PIPE ? NQ : 1][CPL];
-    int2 jk2 = make_int2(0, 0);
-    if (PIPE && e0 < e1) {
-        const float *gj = gbase + (size_t)jk.x * (9 * C);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) ldv<CPL>(gj + q * C, gn[PIPE ? q : 0]);
-        if (e0 + 1 < e1) jk2 = __ldg(ejk + e0 + 1);
-    }
     for (int eb = e0; eb < e1; eb += 8) {
         float pb[8];
 #pragma unroll
@@ -768,26 +760,11 @@ __device__ __forceinline__ void message_bwd_row_part(const TnDev &d, const float
             if (eb + i < e1) {                       // warp-uniform
                 float g[NQ][CPL];
                 const float4 wvc = __ldg(hwV + eb + i), wdc = __ldg(hwD + eb + i);   // land with the gathered row
-                if (PIPE) {
+                const float *gj = gbase + (size_t)jk.x * (9 * C);
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-                        for (int v = 0; v < CPL; ++v) g[q][v] = gn[PIPE ? q : 0][v];
-                    kc.seek(tab, jk.y, cb);
-                    jk = jk2;
-                    if (eb + i + 1 < e1) {
-                        const float *gj = gbase + (size_t)jk.x * (9 * C);
-#pragma unroll
-                        for (int q = 0; q < NQ; ++q) ldv<CPL>(gj + q * C, gn[PIPE ? q : 0]);
-                        if (eb + i + 2 < e1) jk2 = __ldg(ejk + eb + i + 2);
-                    }
-                } else {
-                    const float *gj = gbase + (size_t)jk.x * (9 * C);
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) ldv<CPL>(gj + q * C, g[q]);
-                    kc.seek(tab, jk.y, cb);
-                    if (eb + i + 1 < e1) jk = __ldg(ejk + eb + i + 1);
-                }
+                for (int q = 0; q < NQ; ++q) ldv<CPL>(gj + q * C, g[q]);
+                kc.seek(tab, jk.y, cb);
+                if (eb + i + 1 < e1) jk = __ldg(ejk + eb + i + 1);
                 float p = 0.0f;
 #pragma unroll
                 for (int k = 0; k < NG; ++k) {
@@ -834,9 +811,9 @@ __device__ __forceinline__ void message_bwd_row_part(const TnDev &d, const float
     for (int q = 0; q < NQ; ++q) stv<CPL>(out + q * C, acc[q]);
 }
 
-template <int C, int CPL, bool PIPE>
-__global__ void __launch_bounds__(128, PIPE ? 3 : 4) k_edge_message_bwd_split(TnDev d, int layer, const float *GM,
-                                                                           float *GY, float *gd_layer)
+template <int C, int CPL>
+__global__ void __launch_bounds__(128, 4) k_edge_message_bwd_split(TnDev d, int layer, const float *GM,
+                                                                float *GY, float *gd_layer)
 {
     NNP_PDL_SYNC();
     constexpr int NPARTS = C / (32 * CPL);
@@ -849,8 +826,8 @@ __global__ void __launch_bounds__(128, PIPE ? 3 : 4) k_edge_message_bwd_split(Tn
     const int cb = part * 32 * CPL + lane * CPL;
     const float *tab = d.m.tables + (size_t)(layer + 1) * d.m.num_knots * 6 * C;
     float *gd_slot = gd_layer + (size_t)(2 * part + half) * d.capacity;   // this warp's own slots
-    if (half == 0) message_bwd_row_part<C, CPL, 0, 2, 0, 4, PIPE>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
-    else message_bwd_row_part<C, CPL, 2, 1, 4, 5, PIPE>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
+    if (half == 0) message_bwd_row_part<C, CPL, 0, 2, 0, 4>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
+    else message_bwd_row_part<C, CPL, 2, 1, 4, 5>(d, tab, GM, GY, d.Yc[layer], gd_slot, s, cb);
 }
 
 // ---- sender rows through a shared-memory ring fed by bulk asynchronous copies (TMA engine)
@@ -1985,8 +1962,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("k_node_product_bwd", st); nnp_launch((k_node_product_bwd), NNP_GRID(ew_blocks), 256, 0, st, d.Mc[l], d.Yc[l], GC, GB, d.Qc, n, C); }
         // now GB = G_M, Qc = G_Y (local part)
         if (tune.bwd_split == 2) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_ring<C, CPL>), NNP_GRID(n), 64 * (C / (32 * CPL)), 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else if (tune.bwd_split == 3) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL, true>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
-        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL, false>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
+        else if (tune.bwd_split) { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
         else { NNP_PROF("k_edge_message_bwd", st); EDGE_DISPATCH(C, tune.bwd, (nnp_launch((k_edge_message_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.bwd_block / 32)), tune.bwd_block, 0, st, d, l, GB, d.Qc, d.g_d + (size_t)(1 + l) * d.gd_slots * d.capacity))); }
         // G_Xh = GX + mix^T(G_Y): the sum is formed by the normalisation's reverse, which also writes
         // what the next stage reads - G_D of layer l - 1, or the embedding gate's reverse at layer 0
