@@ -111,6 +111,18 @@ int nnp_distance_pullback(const int32_t *pairs, const double *deltas, const doub
                           const double *g, int32_t count, int32_t n_atoms, double *grad,
                           int32_t *flag_out, nnp_stream_t stream);
 
+/*
+ * distance_pullback_second (neighbors.py:358-380): directional derivative of the pullback along
+ * a position tangent [n_atoms,3], with the analytic pair Hessian (1 - u u^T)/d per edge.
+ *   grad [n_atoms,3] = sum_e +/- g_e (t_ij - u_e (u_e . t_ij)) / d_e,  t_ij = tangent[i] - tangent[j]
+ *   distance_tangent [capacity] = u_e . t_ij on valid rows, 0 on loops and in sentinel slots.
+ * All arrays float64; flag_out as in nnp_distance_pullback.
+ */
+int nnp_distance_pullback_second(const int32_t *pairs, const double *deltas, const double *dists,
+                                 const double *g, const double *tangent, int32_t count,
+                                 int32_t capacity, int32_t n_atoms, double *grad,
+                                 double *distance_tangent, int32_t *flag_out, nnp_stream_t stream);
+
 /* ------------------------------------------------------------------ TensorNet step
  * Replaces GraphPotential.evaluate (graphnet.py:567-580) = forward (graphnet.py:317-412) +
  * backward_forces (graphnet.py:516-537) with the TensorNet arithmetic of SURVEY.md

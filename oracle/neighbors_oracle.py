@@ -326,6 +326,33 @@ def distance_pullback(pairs, deltas, distances, count, n_atoms, d_grad):
     return segment_sum(contrib, pairs[:, 0], n_atoms) - segment_sum(contrib, pairs[:, 1], n_atoms)
 
 
+def distance_pullback_second(pairs, deltas, distances, count, n_atoms, capacity, d_grad, position_tangent):
+    """Directional derivative of distance_pullback along a position tangent with the analytic pair
+    Hessian (I - u u^T)/d; also the distance tangents u . (t_i - t_j), zero on loops and in sentinel
+    slots (neighbors.py:358-380, same operation order)."""
+    pairs = np.asarray(pairs)[:count]
+    deltas = np.asarray(deltas, dtype=np.float64)[:count]
+    dists = np.asarray(distances, dtype=np.float64)[:count]
+    g = np.asarray(d_grad, dtype=np.float64)[:count]
+    tangent = np.asarray(position_tangent, dtype=np.float64)
+    loops = pairs[:, 0] == pairs[:, 1]
+    bad = ~loops & (dists == 0.0)
+    if np.any(bad):
+        i, j = pairs[bad][0]
+        raise OracleNumericError(f"zero-distance pair ({i}, {j}) has no defined distance direction")
+    safe = np.where(loops, 1.0, dists)
+    unit = deltas / safe[:, None]
+    unit[loops] = 0.0
+    tdiff = tangent[pairs[:, 0]] - tangent[pairs[:, 1]]
+    ddot = np.einsum("ij,ij->i", unit, tdiff)
+    hvp = g[:, None] * (tdiff - unit * ddot[:, None]) / safe[:, None]
+    hvp[loops] = 0.0
+    grad = segment_sum(hvp, pairs[:, 0], n_atoms) - segment_sum(hvp, pairs[:, 1], n_atoms)
+    distance_tangent = np.zeros(capacity)
+    distance_tangent[:count] = np.where(loops, 0.0, ddot)
+    return grad, distance_tangent
+
+
 # ------------------------------------------------------- independent O(N^2) oracle
 
 _IMAGE_SHIFTS = np.array(

@@ -10,6 +10,7 @@ from .radial import cosine_cutoff, cosine_cutoff_grad, expnorm_initial_params, r
 from .neighbors import (
     NeighborList, NeighborSpec, as_full_list, as_half_list, build_neighbor_list,
     build_with_auto_capacity, canonicalize, capacity_heuristic, distance_pullback,
+    distance_pullback_second,
 )
 from .tensornet import TNConfig, TensorNet, build_radial_tables, init_params
 from .priors import Atomref, Coulomb, D2Dispersion, PriorStack, PriorTerm, ZBL, evaluate_prior_stack

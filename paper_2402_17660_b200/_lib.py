@@ -25,7 +25,7 @@ TN_MAX_LAYERS = 8
 
 EXPORTED_SYMBOLS = (
     "nnp_last_error", "nnp_version", "nnp_abi_sizeof", "nnp_nl_workspace_bytes", "nnp_nl_build", "nnp_f32_to_f64",
-    "nnp_distance_pullback", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
+    "nnp_distance_pullback", "nnp_distance_pullback_second", "nnp_tn_workspace_bytes", "nnp_tn_energy_forces",
     "nnp_test_gemm_nt", "nnp_set_gemm_mode", "nnp_launch_count", "nnp_profile_begin",
     "nnp_profile_report", "nnp_md_langevin_middle", "nnp_priors_pair_terms",
 )
@@ -110,6 +110,7 @@ def load() -> ctypes.CDLL:
     lib.nnp_nl_build.argtypes = [ctypes.POINTER(NlParams), _p, _p, _p, _p, _p, _p, _p, _p, _p, sz, _p]
     lib.nnp_f32_to_f64.argtypes = [_p, _p, ctypes.c_int64, _p]
     lib.nnp_distance_pullback.argtypes = [_p, _p, _p, _p, _i32, _i32, _p, _p, _p]
+    lib.nnp_distance_pullback_second.argtypes = [_p, _p, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p]
     lib.nnp_tn_workspace_bytes.argtypes = [ctypes.POINTER(TnModel), _i32, _i32, _i32, ctypes.POINTER(sz)]
     lib.nnp_tn_energy_forces.argtypes = [
         ctypes.POINTER(TnModel), _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, sz, _p,

@@ -890,6 +890,67 @@ extern "C" int nnp_f32_to_f64(const float *src, double *dst, int64_t n, nnp_stre
     return NNP_OK;
 }
 
+// Directional derivative of the pullback along a position tangent (neighbors.py:358-380): per edge
+// the pair Hessian (1 - u u^T)/d applied to t_i - t_j, scattered +/- like the pullback itself, and
+// the distance tangent u . (t_i - t_j) (zero on loops; the caller pre-zeroes the sentinel tail).
+// Operation order as the reference: tdiff, ddot = sum_k u_k tdiff_k (left to right),
+// hvp_k = g * (tdiff_k - u_k * ddot) / d.
+__global__ void k_pullback_second(const int *__restrict__ pairs, const double *__restrict__ deltas,
+                                  const double *__restrict__ dists, const double *__restrict__ g,
+                                  const double *__restrict__ tangent, int count, double *__restrict__ grad,
+                                  double *__restrict__ dtan, int *__restrict__ flag)
+{
+    NNP_PDL_SYNC();
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    int i = pairs[2 * e], j = pairs[2 * e + 1];
+    if (i < 0) return;
+    if (i == j) {
+        dtan[e] = 0.0;
+        return;
+    }
+    double d = dists[e];
+    if (d == 0.0) {
+        atomicMin(flag, e + 1);
+        return;
+    }
+    double u[3], td[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        u[k] = deltas[3 * (size_t)e + k] / d;
+        td[k] = __dsub_rn(tangent[3 * (size_t)i + k], tangent[3 * (size_t)j + k]);
+    }
+    const double ddot = __dadd_rn(__dadd_rn(__dmul_rn(u[0], td[0]), __dmul_rn(u[1], td[1])), __dmul_rn(u[2], td[2]));
+    dtan[e] = ddot;
+    const double ge = g[e];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double c = __dmul_rn(ge, __dsub_rn(td[k], __dmul_rn(u[k], ddot))) / d;
+        atomicAdd(&grad[3 * (size_t)i + k], c);
+        atomicAdd(&grad[3 * (size_t)j + k], -c);
+    }
+}
+
+extern "C" int nnp_distance_pullback_second(const int32_t *pairs, const double *deltas, const double *dists,
+                                            const double *g, const double *tangent, int32_t count,
+                                            int32_t capacity, int32_t n_atoms, double *grad,
+                                            double *distance_tangent, int32_t *flag_out, nnp_stream_t stream_)
+{
+    NNP_CHECK_ARG(grad && distance_tangent && flag_out && tangent && count >= 0 && capacity >= count && n_atoms >= 1,
+                  "bad arguments to nnp_distance_pullback_second");
+    NNP_CHECK_ARG(count == 0 || (pairs && deltas && dists && g),
+                  "NULL edge buffer passed to nnp_distance_pullback_second");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    cudaMemsetAsync(grad, 0, 3 * (size_t)n_atoms * sizeof(double), stream);
+    cudaMemsetAsync(distance_tangent, 0, (size_t)capacity * sizeof(double), stream);
+    cudaMemsetAsync(flag_out, 0x7f, sizeof(int), stream);
+    if (count > 0)
+        nnp_launch((k_pullback_second), NNP_GRID(nnp_blocks(count, 256)), 256, 0, stream, pairs, deltas, dists, g,
+                   tangent, count, grad, distance_tangent, flag_out);
+    NNP_CHECK_LAUNCH("distance_pullback_second");
+    return NNP_OK;
+}
+
 extern "C" int nnp_distance_pullback(const int32_t *pairs, const double *deltas,
                                      const double *dists, const double *g, int32_t count,
                                      int32_t n_atoms, double *grad, int32_t *flag_out,

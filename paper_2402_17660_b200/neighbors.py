@@ -323,3 +323,46 @@ def distance_pullback(nlist: NeighborList, d_grad) -> np.ndarray:
         i, j = (int(x) for x in pairs[bad - 1].tolist())
         raise NumericError(f"zero-distance pair ({i}, {j}) has no defined distance direction")
     return grad.cpu().numpy()
+
+
+def distance_pullback_second(nlist: NeighborList, d_grad, position_tangent):
+    """Directional derivative of ``distance_pullback`` along a position tangent, on the GPU
+    (neighbors.py:358-380): the analytic pair Hessian (I - u u^T)/d per edge.  Returns
+    ``(grad [n_atoms, 3], distance_tangent [capacity])`` as numpy float64 arrays; the distance
+    tangents u . (t_i - t_j) are zero on loops and in sentinel slots."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    position_tangent = np.asarray(position_tangent, dtype=np.float64)
+    if position_tangent.shape != (nlist.n_atoms, 3):
+        raise ValidationError(f"position tangent must have shape ({nlist.n_atoms}, 3)")
+    d_grad = np.asarray(d_grad, dtype=np.float64)
+    if d_grad.shape not in ((nlist.capacity,), (nlist.count,)):
+        raise ValidationError(
+            f"d_grad must have capacity ({nlist.capacity}) or count "
+            f"({nlist.count}) entries, got {d_grad.shape}"
+        )
+    dev = torch.device("cuda")
+
+    def to_dev(a, dtype):
+        if isinstance(a, np.ndarray):
+            return torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+        return a.to(dtype=dtype).contiguous()
+
+    pairs = to_dev(nlist.pairs, torch.int32)
+    deltas = to_dev(nlist.deltas, torch.float64)
+    dists = to_dev(nlist.distances, torch.float64)
+    g = torch.as_tensor(np.ascontiguousarray(d_grad[: nlist.count])).to(dev)
+    tangent = torch.as_tensor(np.ascontiguousarray(position_tangent)).to(dev)
+    grad = torch.empty((nlist.n_atoms, 3), dtype=torch.float64, device=dev)
+    dtan = torch.empty(nlist.capacity, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    rc = lib.nnp_distance_pullback_second(
+        _lib.ptr(pairs), _lib.ptr(deltas), _lib.ptr(dists), _lib.ptr(g), _lib.ptr(tangent), nlist.count,
+        nlist.capacity, nlist.n_atoms, _lib.ptr(grad), _lib.ptr(dtan), _lib.ptr(flag), _lib.current_stream())
+    _lib.check(rc, "nnp_distance_pullback_second")
+    bad = int(flag.item())
+    if bad != 0x7F7F7F7F:
+        i, j = (int(x) for x in pairs[bad - 1].tolist())
+        raise NumericError(f"zero-distance pair ({i}, {j}) has no defined distance direction")
+    return grad.cpu().numpy(), dtan.cpu().numpy()
+

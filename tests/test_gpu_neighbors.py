@@ -237,6 +237,43 @@ def test_full_size_sweep_point_properties():
     assert np.array_equal(fp[:, 0], np.repeat(np.arange(n), np.diff(rp)))
 
 
+def test_second_order_pullback_against_reference_golden(golden):
+    """distance_pullback_second (neighbors.py:358-380) on device lists against outputs of the
+    reference's own function (tests/golden/pullback2_golden.npz): gradient to 1e-12 (float64 atomics
+    change the summation order), distance tangents to 1e-14, sentinel tail zero; same errors."""
+    import os
+
+    arrays, manifest = golden
+    p2 = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pullback2_golden.npz"))
+    cases = {c["key"]: c for c in manifest["cases"]}
+    for key in (str(k) for k in p2["keys"]):
+        case = cases[key]
+        box = arrays[f"{key}_box"] if f"{key}_box" in arrays.files else None
+        system = make_system(arrays[f"{key}_pos"], arrays[f"{key}_batch"], box)
+        nl = P.build_neighbor_list(system, P.NeighborSpec(
+            cutoff_upper=case["cutoff_upper"], cutoff_lower=case["cutoff_lower"], capacity=case["capacity"],
+            strategy=case["strategy"], full_list=case["full_list"], include_self_loops=case["include_self_loops"]))
+        grad, dtan = P.distance_pullback_second(nl, p2[f"{key}_g"], p2[f"{key}_tangent"])
+        ref = p2[f"{key}_grad"]
+        assert grad.shape == ref.shape and dtan.shape == (case["capacity"],)
+        assert np.max(np.abs(grad - ref), initial=0.0) <= 1e-12 * max(np.max(np.abs(ref), initial=0.0), 1.0), key
+        assert np.max(np.abs(dtan[: nl.count] - p2[f"{key}_dtan"]), initial=0.0) < 1e-14, key
+        assert not np.any(dtan[nl.count:]), key
+    # the host copy of a list works as well, and the reference's validation errors are kept
+    host = nl.as_reference()
+    g2, t2 = P.distance_pullback_second(host, p2[f"{key}_g"], p2[f"{key}_tangent"])
+    assert np.allclose(g2, grad, rtol=0, atol=1e-12) and np.array_equal(t2, dtan)
+    with pytest.raises(P.ValidationError, match="position tangent"):
+        P.distance_pullback_second(nl, p2[f"{key}_g"], np.zeros((3, 3)))
+    with pytest.raises(P.ValidationError, match="d_grad"):
+        P.distance_pullback_second(nl, np.zeros(nl.count + 1), p2[f"{key}_tangent"])
+    pos = np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    coincident = P.build_neighbor_list(make_system(pos, None, None), P.NeighborSpec(cutoff_upper=2.0, capacity=8))
+    if coincident.count == 3:       # the zero-distance pair is listed when the lower cutoff admits it
+        with pytest.raises(P.NumericError, match="zero-distance"):
+            P.distance_pullback_second(coincident, np.ones(8), np.ones((3, 3)))
+
+
 def test_one_million_atoms_bit_exact():
     """1 048 576 atoms (the largest point of config B's sweep): pairs, deltas and distances of the
     half list equal the C oracle's bit for bit (the oracle needs a few seconds on one core)."""

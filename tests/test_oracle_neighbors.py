@@ -156,3 +156,27 @@ def test_pullback_single_pair_and_zero_distance():
     assert np.allclose(g, [[1.0, 0, 0], [-1.0, 0, 0]])
     with pytest.raises(O.OracleNumericError, match=r"zero-distance pair \(0, 1\)"):
         O.distance_pullback(np.array([[0, 1]]), np.zeros((1, 3)), np.zeros(1), 1, 2, np.ones(1))
+
+
+def test_second_order_pullback_oracle_matches_reference_golden():
+    """oracle.distance_pullback_second against outputs of the reference's own function
+    (tests/golden/make_pullback2_golden.py) on 32 of the golden lists: bit-exact."""
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    arrays = np.load(os.path.join(here, "neighbors_golden.npz"))
+    p2 = np.load(os.path.join(here, "pullback2_golden.npz"))
+    manifest = json.load(open(os.path.join(here, "neighbors_golden.json")))
+    cases = {c["key"]: c for c in manifest["cases"]}
+    assert len(p2["keys"]) == 32
+    for key in p2["keys"]:
+        key = str(key)
+        case = cases[key]
+        pairs, deltas, dists = arrays[f"{key}_pairs"], arrays[f"{key}_deltas"], arrays[f"{key}_dists"]
+        n = len(arrays[f"{key}_pos"])
+        grad, dtan = O.distance_pullback_second(pairs, deltas, dists, case["count"], n, case["capacity"],
+                                                p2[f"{key}_g"], p2[f"{key}_tangent"])
+        assert np.array_equal(grad, p2[f"{key}_grad"]), key
+        assert np.array_equal(dtan[: case["count"]], p2[f"{key}_dtan"]), key
+        assert dtan.shape == (case["capacity"],) and not np.any(dtan[case["count"]:])
