@@ -90,6 +90,7 @@ struct TnDev {
     int2 *ejk;     // (sender j, knot interval kn)
     float4 *hwV;   // weights of f_e * phi_e
     float4 *hwD;   // weights of d(f_e * phi_e)/dd = f' * dtx/dd * phi + f * phi'
+    int *ezs;      // species of the edge's sender (the embedding reads z_send[ezs[e]])
     float *g_d;    // [(L+1) * gd_slots][capacity] dE/dd_e: one slot per (writing kernel, channel part), so every
                    // kernel stores its share without a read-modify-write; summed in k_forces
     float4 *g_u;   // [NNP_PARTS][capacity] dE/du_e
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(256) k_edge_order(TnDev d)
             const float dr0 = fmaf(h.d01, su, h.h01 * dphi), dr1 = fmaf(h.d11, su, h.h11 * dphi);
             const bool even = (kn & 1) == 0;                   // the interval's left knot is the even one
             d.ejk[p] = make_int2(j, kn);
+            d.ezs[p] = d.zs[j];
             d.hwV[p] = even ? make_float4(l0, l1, r0, r1) : make_float4(r0, r1, l0, l1);
             d.hwD[p] = even ? make_float4(dl0, dl1, dr0, dr1) : make_float4(dr0, dr1, dl0, dl1);
         }
@@ -600,6 +602,107 @@ struct KnotEO {
             f[v] = fmaf(w.x, ev[k][v], fmaf(w.y, em[k][v], fmaf(w.z, ov[k][v], w.w * om[k][v])));
     }
 };
+
+// The embedding's edge sum as two knot-cached warps per (receiver, channel part), like the message
+// kernel: X0_i[q] = sum_e (dp_g(q)(d_e) phi_e) (z_recv[z_i] + z_send[z_j]) b_q(u_e).  The radial part
+// comes from the interval's two knots in registers and the per-edge weights of k_edge_order (table 0,
+// envelope folded in), the species factor from the sender-species record, so an edge costs one
+// 16-byte table-row read instead of twelve coefficient loads.
+template <int C, int CPL, int K0, int NG, int Q0, int NQ>
+__device__ __forceinline__ void embed_row_part(const TnDev &d, int s, int cb, float (&acc)[NQ][CPL])
+{
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) acc[q][v] = 0.0f;
+    float zr[CPL];
+    ldv<CPL>(d.m.z_recv + (size_t)d.zs[s] * C + cb, zr);
+    const float *tab = d.m.tables;                      // table 0: the three distance projections
+    const int e0 = d.row_ptr[s], e1 = d.row_ptr[s + 1];
+    KnotEO<C, CPL, K0, NG> kc;
+    kc.init();
+    const int2 *__restrict__ ejk = d.ejk;
+    const float4 *__restrict__ hwV = d.hwV;
+    const float4 *__restrict__ geoB = d.geoB;
+    const int *__restrict__ ezs = d.ezs;
+    const float *zsend = d.m.z_send + cb;
+    int kn = e0 < e1 ? __ldg(ejk + e0).y : 0;
+    int zj = e0 < e1 ? __ldg(ezs + e0) : 0;
+    for (int e = e0; e < e1; ++e) {
+        float zs[CPL];
+        ldv<CPL>(zsend + (size_t)zj * C, zs);
+        const float4 wc = __ldg(hwV + e);
+        const float4 gb = __ldg(geoB + e);
+        kc.seek(tab, kn, cb);
+        if (e + 1 < e1) {
+            kn = __ldg(ejk + e + 1).y;
+            zj = __ldg(ezs + e + 1);
+        }
+        float b[9];
+        edge_basis9(gb.x, gb.y, gb.z, b);
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            float f[CPL];
+            kc.eval(wc, k, f);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) f[v] *= zr[v] + zs[v];
+            const int g = K0 + k;
+            const int qa = (g == 0 ? 0 : (g == 1 ? 1 : 4)), qb = (g == 0 ? 1 : (g == 1 ? 4 : 9));
+#pragma unroll
+            for (int q = qa; q < qb; ++q)
+#pragma unroll
+                for (int v = 0; v < CPL; ++v) acc[q - Q0][v] = fmaf(f[v], b[q], acc[q - Q0][v]);
+        }
+    }
+    float *out = d.X0 + ((size_t)s * 9 + Q0) * C + cb;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) stv<CPL>(out + q * C, acc[q]);
+}
+
+// launched with blocks of 64 * k threads: the two halves of a (receiver, part) are neighbouring warps
+template <int C, int CPL>
+__global__ void __launch_bounds__(128, 5) k_embed_edge_split(TnDev d)
+{
+    NNP_PDL_SYNC();
+    constexpr int NPARTS = C / (32 * CPL);
+    __shared__ float s_norm[4][32 * CPL];               // S-half partial of |X0|^2, per warp of the block
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    const int s = gw / (2 * NPARTS), rem = gw - s * (2 * NPARTS);
+    const int part = rem >> 1, half = rem & 1;
+    const bool live = s < d.n;
+    const int cb = part * 32 * CPL + lane * CPL;
+    float nrm[CPL];
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) nrm[v] = 0.0f;
+    if (live) {
+        if (half == 0) {
+            float acc[4][CPL];
+            embed_row_part<C, CPL, 0, 2, 0, 4>(d, s, cb, acc);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v)       // <X,X>_I + <X,X>_A = 3 s^2 + 2 |a|^2
+                nrm[v] = 3.0f * acc[0][v] * acc[0][v] +
+                         2.0f * (acc[1][v] * acc[1][v] + acc[2][v] * acc[2][v] + acc[3][v] * acc[3][v]);
+        } else {
+            float acc[5][CPL];
+            embed_row_part<C, CPL, 2, 1, 4, 5>(d, s, cb, acc);
+#pragma unroll
+            for (int v = 0; v < CPL; ++v) {     // <X,X>_S with Szz = -Sxx - Syy
+                const float szz = acc[0][v] + acc[1][v];
+                nrm[v] = acc[0][v] * acc[0][v] + acc[1][v] * acc[1][v] + szz * szz +
+                         2.0f * (acc[2][v] * acc[2][v] + acc[3][v] * acc[3][v] + acc[4][v] * acc[4][v]);
+                s_norm[wib][lane * CPL + v] = nrm[v];
+            }
+        }
+    }
+    __syncthreads();
+    if (live && half == 0) {
+#pragma unroll
+        for (int v = 0; v < CPL; ++v) nrm[v] += s_norm[wib + 1][lane * CPL + v];
+        stv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+    }
+}
 
 // One warp's share of a receiver row: components [Q0, Q0 + NQ) = radial groups [K0, K0 + NG).
 template <int C, int CPL, int K0, int NG, int Q0, int NQ>
@@ -1724,6 +1827,7 @@ size_t carve(TnDev &d, void *ws)
     d.ejk = ar.take<int2>(cap);
     d.hwV = ar.take<float4>(cap);
     d.hwD = ar.take<float4>(cap);
+    d.ezs = ar.take<int>(cap);
     d.g_d = ar.take<float>(cap * NNP_GD_SLOTS * (size_t)(L + 1));
     d.g_u = ar.take<float4>(cap * NNP_PARTS);
     d.zs = ar.take<int>(n);
@@ -1835,7 +1939,7 @@ GemmBatch mix_gemm(const float *A, const nnp_gemm_weight *W3, float *out, int n,
 // node's row).  Fewer channels per lane = fewer registers and more warps in flight; tunable
 // through NNP_CPL_{EMB,FWD,BWD,EMBBWD} for measurements.
 struct EdgeTuning {
-    int emb, fwd, bwd, embbwd, bwd_block, fwd_block, emb_block, bwd_split;
+    int emb, fwd, bwd, embbwd, bwd_block, fwd_block, emb_block, bwd_split, emb_split;
 };
 static int env_int(const char *name, int fallback)
 {
@@ -1847,8 +1951,9 @@ static const EdgeTuning &edge_tuning()
     static const EdgeTuning t = {env_int("NNP_CPL_EMB", 4), env_int("NNP_CPL_FWD", 4),
                                  env_int("NNP_CPL_BWD", 4), env_int("NNP_CPL_EMBBWD", 4),
                                  std::min(env_int("NNP_BWD_BLOCK", 128), 128), std::min(env_int("NNP_FWD_BLOCK", 64), 128), env_int("NNP_EMB_BLOCK", 128),
-                                 env_int("NNP_BWD_SPLIT", 1)};   // 1 = register gather, two warps per receiver (default); 2 = bulk-copy ring
+                                 env_int("NNP_BWD_SPLIT", 1),   // 1 = register gather, two warps per receiver (default); 2 = bulk-copy ring
                                                                 // (measured slower: 2.15 vs 1.30 ms per step); 0 = one warp per part, monomial tables
+                                 env_int("NNP_EMB_SPLIT", 2)};  // knot-cached two-warp embedding edge kernel: 1 = always, 0 = never, 2 = up to 2 048 atoms
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -1895,7 +2000,10 @@ int run_step(TnDev &d, cudaStream_t st)
     if (d.m.embed_projection && d.forces) { NNP_PROF("k_embed_slots", st); nnp_launch((k_embed_slots), NNP_GRID(3 * 2 * EMB_SLOTS), 256, 0, st, d); }
 
     // ---- embedding
-    { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d))); }
+    // two knot-cached warps per receiver pay off for small systems only (measured: 22 atoms 14.2 vs
+    // 21.6 us; config C 0.343 vs 0.338 ms; config D 1.01 vs 0.88 ms): NNP_EMB_SPLIT = 2 picks by size
+    if (tune.emb_split == 1 || (tune.emb_split == 2 && n <= 2048)) { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), 2)), 64, 0, st, d))); }
+    else { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d))); }
     { NNP_PROF("k_embed_ln", st); nnp_launch((k_embed_ln<C>), NNP_GRID(warp_blocks), 256, 0, st, d); }
     {
         GemmBatch b{};
