@@ -3,7 +3,7 @@ cutoff neighbor search + TensorNet energy-and-forces step, as hand-written sm_10
 the C ABI of ``include/nnp_b200.h``.  Names follow ``nnpkit/__init__.py`` for this path."""
 
 from .errors import (
-    CapacityError, DataError, ExtensionError, NumericError, ToolkitError, ValidationError,
+    CapacityError, DataError, ExtensionError, NumericError, ParseError, ToolkitError, ValidationError,
 )
 from .system import Box, EnergyForces, System, build_system, minimum_image
 from .radial import cosine_cutoff, cosine_cutoff_grad, expnorm_initial_params, rbf_expnorm
@@ -19,5 +19,7 @@ from .md import (
     MDState, Trajectory, default_masses, initialize_state, langevin_middle_step,
     maxwell_boltzmann_velocities, rmsd, run_simulation, throughput,
 )
+
+from .structio import Frame, load_extxyz, load_structure, load_weights, save_weights, write_extxyz
 
 __version__ = "0.1.0"

@@ -280,6 +280,21 @@ class TensorNet:
         self._model = m
         self._weights = keep
 
+    # ---------------------------------------------------------------- weights on disk
+    def save(self, path) -> None:
+        """Write config and weights (structio.save_weights)."""
+        from .structio import save_weights
+
+        save_weights(path, self.config, self.params)
+
+    @classmethod
+    def load(cls, path, **kwargs) -> "TensorNet":
+        """A model from a file written by ``save``."""
+        from .structio import load_weights
+
+        config, params = load_weights(path)
+        return cls(config=config, params=params, **kwargs)
+
     # -------------------------------------------------------------------- plans
     def neighbor_capacity(self, n_atoms: int) -> int:
         """Directed rows incl. self loops: 2*N*max_num_neighbors, as compose.py:59-71 sizes a

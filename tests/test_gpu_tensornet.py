@@ -293,6 +293,23 @@ def test_gemm_engine_is_per_model_and_thread_safe(rng):
         P.TensorNet(gemm_mode=2, **kw)
 
 
+def test_saved_weights_and_a_structure_file_reproduce_the_model(tmp_path, rng):
+    """TensorNet.save / TensorNet.load (structio weights container) and load_structure: the reloaded
+    model gives bit-identical energies and forces on a structure read back from an XYZ file."""
+    z, pos, _, _ = small_open(rng, 18)
+    P.write_extxyz(tmp_path / "mol.xyz", [P.Frame(positions=pos, species=np.where(z == 7, 8, z).astype(np.int64), energy=0.0)])
+    pos2, z2 = P.load_structure(tmp_path / "mol.xyz")
+    assert np.array_equal(pos2, pos)
+    a = P.TensorNet(embedding_dimension=64, num_layers=2, num_rbf=16, cutoff_upper=4.5, max_z=12, mean=0.1, std=2.0, seed=8)
+    a.save(tmp_path / "model.tnw")
+    b = P.TensorNet.load(tmp_path / "model.tnw")
+    assert b.config == a.config
+    args = (torch.as_tensor(z2), torch.as_tensor(pos2, dtype=torch.float32))
+    e1, f1 = a(*args)
+    e2, f2 = b(*args)
+    assert torch.equal(e1, e2) and torch.equal(f1, f2)
+
+
 def test_invariances_on_device(rng):
     z, pos, batch, _ = small_open(rng, 26)
     model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=2)
