@@ -224,12 +224,17 @@ int nnp_tn_energy_forces(const nnp_tn_model *m, int32_t n_atoms, int32_t n_sampl
  *              the random stream by itself
  *   c1 = exp(-gamma dt), c2 = sqrt(1 - c1^2) (md.py:128-129); c2 == 0 skips the mixing
  *   pos32_out  optional [n,3] float32 copy of the new positions
- *   nonfinite_flag optional device int32, set to 1 when a force is not finite (md.py:124-125)
+ *   nonfinite_flag optional device int32, set to 1 when a force is not finite (md.py:124-125) and to
+ *              2 when the step was frozen because of a neighbor overflow
+ *   nl_counts, nl_capacity: optional counts of the nnp_nl_build that fed this step; when
+ *              nl_counts[0] > nl_capacity the forces are stale, so positions, velocities and the
+ *              step counter are left untouched (the caller regrows the list and repeats the step)
  */
 int nnp_md_langevin_middle(double *pos, double *vel, const float *forces, const double *acc_scale,
                            const double *sigma, const double *noise, uint64_t seed,
                            uint64_t *step_counter, double dt, double c1, double c2,
-                           float *pos32_out, int32_t *nonfinite_flag, int32_t n, nnp_stream_t stream);
+                           float *pos32_out, int32_t *nonfinite_flag, int32_t n,
+                           const int32_t *nl_counts, int32_t nl_capacity, nnp_stream_t stream);
 
 /* ------------------------------------------------------------------ analytic pair priors
  * Replaces the pair functions and the assembly of priors.py:61-88,139-148,170-185,222-245 on a

@@ -120,7 +120,7 @@ def load() -> ctypes.CDLL:
     dbl, u64 = ctypes.c_double, ctypes.c_uint64
     lib.nnp_priors_pair_terms.argtypes = [ctypes.POINTER(PriorParams), _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _p,
                                           _i32, _p, _p, _p]
-    lib.nnp_md_langevin_middle.argtypes = [_p, _p, _p, _p, _p, _p, u64, _p, dbl, dbl, dbl, _p, _p, _i32, _p]
+    lib.nnp_md_langevin_middle.argtypes = [_p, _p, _p, _p, _p, _p, u64, _p, dbl, dbl, dbl, _p, _p, _i32, _p, _i32, _p]
     lib.nnp_launch_count.argtypes = [ctypes.c_int]
     lib.nnp_profile_begin.argtypes = []
     lib.nnp_profile_report.argtypes = [ctypes.c_char_p, ctypes.c_int]

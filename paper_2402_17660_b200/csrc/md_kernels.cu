@@ -54,9 +54,17 @@ __global__ void k_langevin_middle(double *__restrict__ pos, double *__restrict__
                                   const double *__restrict__ sigma, const double *__restrict__ noise,
                                   unsigned long long seed, const unsigned long long *__restrict__ step_counter,
                                   double dt, double c1, double c2, float *__restrict__ pos32_out,
-                                  int *__restrict__ flag, int n)
+                                  int *__restrict__ flag, int n, const int *__restrict__ nl_counts,
+                                  int nl_capacity)
 {
     NNP_PDL_SYNC();
+    // The neighbor structure overflowed in this step: the energy/forces kernels returned early and
+    // `forces` still holds the previous step's values.  Freeze the state instead of integrating stale
+    // forces (flag 2; the host regrows the list and resumes from here).
+    if (nl_counts && nl_counts[0] > nl_capacity) {
+        if (flag && blockIdx.x == 0 && threadIdx.x == 0) atomicMax(flag, 2);
+        return;
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double half_dt = 0.5 * dt;
@@ -112,9 +120,10 @@ __global__ void k_langevin_middle(double *__restrict__ pos, double *__restrict__
     if (!finite && flag) atomicMax(flag, 1);
 }
 
-__global__ void k_advance_counter(unsigned long long *counter)
+__global__ void k_advance_counter(unsigned long long *counter, const int *__restrict__ nl_counts, int nl_capacity)
 {
     NNP_PDL_SYNC();
+    if (nl_counts && nl_counts[0] > nl_capacity) return;     // frozen step: the random stream does not advance
     counter[0] += 1ull;
 }
 
@@ -124,16 +133,18 @@ extern "C" int nnp_md_langevin_middle(double *pos, double *vel, const float *for
                                       const double *sigma, const double *noise, uint64_t seed,
                                       uint64_t *step_counter, double dt, double c1, double c2,
                                       float *pos32_out, int32_t *nonfinite_flag, int32_t n,
-                                      nnp_stream_t stream)
+                                      const int32_t *nl_counts, int32_t nl_capacity, nnp_stream_t stream)
 {
     NNP_CHECK_ARG(pos && vel && forces && acc_scale && sigma && n >= 1, "bad arguments to nnp_md_langevin_middle");
     NNP_CHECK_ARG(dt > 0.0 && c1 >= 0.0 && c1 <= 1.0 && c2 >= 0.0, "bad integrator coefficients");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     nnp_launch((k_langevin_middle), NNP_GRID(nnp_blocks(n, 256)), 256, 0, st, 
         pos, vel, forces, acc_scale, sigma, noise, (unsigned long long)seed,
-        reinterpret_cast<const unsigned long long *>(step_counter), dt, c1, c2, pos32_out, nonfinite_flag, n);
+        reinterpret_cast<const unsigned long long *>(step_counter), dt, c1, c2, pos32_out, nonfinite_flag, n,
+        nl_counts, nl_capacity);
     if (step_counter)
-        nnp_launch((k_advance_counter), NNP_GRID(1), 1, 0, st, reinterpret_cast<unsigned long long *>(step_counter));
+        nnp_launch((k_advance_counter), NNP_GRID(1), 1, 0, st, reinterpret_cast<unsigned long long *>(step_counter),
+                   nl_counts, nl_capacity);
     NNP_CHECK_LAUNCH("langevin_middle");
     return NNP_OK;
 }

@@ -100,7 +100,7 @@ extern "C" int nnp_profile_report(char *buf, int buf_bytes)
     }
     return NNP_OK;
 }
-extern "C" int nnp_version(void) { return 101; }
+extern "C" int nnp_version(void) { return 102; }
 extern "C" int nnp_abi_sizeof(int which)
 {
     switch (which) {

@@ -143,13 +143,18 @@ class DeviceIntegrator:
     position buffer, so the step graph reads what the integrator wrote."""
 
     def __init__(self, model, system: System, velocities: np.ndarray, masses: np.ndarray,
-                 temperature: float, seed: int = 0):
+                 temperature: float, seed: int = 0, max_num_neighbors: Optional[int] = None):
         torch = _lib.require_cuda()
         self.torch, self.model, self.lib = torch, model, _lib.load()
         dev = model.device
         n = system.n_atoms
         self.n = n
         self.system = system
+        if max_num_neighbors is not None and max_num_neighbors != model.config.max_num_neighbors:
+            # the reference sizes the list from this argument (md.py:107-111 -> compose.py:59-71):
+            # directed rows incl. self loops = 2 * N * max_num_neighbors; a larger learned size wins
+            key = (n, system.n_samples)
+            model._capacity_hint[key] = max(model._capacity_hint.get(key, 0), 2 * n * int(max_num_neighbors))
         # one checked float64 step creates (and captures) the plan whose pos64 buffer we own
         model.forward(system.species, system.positions, system.batch if system.n_samples > 1 else None,
                       system.box, n_samples=system.n_samples, check=True, clone=False)
@@ -173,7 +178,8 @@ class DeviceIntegrator:
             _lib.ptr(p.pos64), _lib.ptr(self.vel), _lib.ptr(p.forces), _lib.ptr(self.acc_scale),
             _lib.ptr(self.sigma), None if device_noise else _lib.ptr(self.noise),
             ctypes.c_uint64(self.seed), _lib.ptr(self.counter) if device_noise else None,
-            dt, c1, c2, None, _lib.ptr(self.flag), self.n, _lib.current_stream())
+            dt, c1, c2, None, _lib.ptr(self.flag), self.n, _lib.ptr(p.engine.counts), p.capacity,
+            _lib.current_stream())
         _lib.check(rc, "nnp_md_langevin_middle")
 
     def step_with_noise(self, dt_fs, gamma_per_ps, noise: Optional[np.ndarray]) -> None:
@@ -223,13 +229,36 @@ class DeviceIntegrator:
         return float(self.plan.energy.sum().item())
 
     def check_finite(self, what: str) -> None:
-        if int(self.flag.item()) != 0:
+        """NumericError on non-finite forces; CapacityError when a step found more neighbor rows than
+        the plan holds.  In that case the integrator kernel froze the state at the last good step
+        (positions, velocities and the noise counter untouched), so ``regrow`` + more steps resume it."""
+        flag = int(self.flag.item())
+        if flag == 1:
             raise NumericError(f"non-finite forces {what}")
         required = int(self.plan.engine.counts[0].item())
-        if required > self.plan.capacity:
+        if flag == 2 or required > self.plan.capacity:
             from .errors import CapacityError
 
             raise CapacityError(required=required, capacity=self.plan.capacity)
+
+    def steps_done(self) -> int:
+        """Integrator steps actually taken by ``run_device`` so far (frozen steps do not count)."""
+        return int(self.counter.item())
+
+    def regrow(self) -> None:
+        """After a CapacityError: a plan with room for the rows the frozen step asked for (the model's
+        own overflow loop, neighbors.py:238-247), the state carried over, graphs re-captured lazily."""
+        torch = self.torch
+        positions = self.plan.pos64.clone()
+        s = self.system
+        self.model.forward(s.species, positions, s.batch if s.n_samples > 1 else None, s.box,
+                           n_samples=s.n_samples, check=True, clone=False)
+        self.plan = self.model._last_plan
+        self.plan.pos64.copy_(positions)
+        self.flag.zero_()
+        self.graph, self._graph_key = None, None
+        self._forces_current = True
+        torch.cuda.synchronize(self.model.device)
 
 
 def network_of(potential):
@@ -255,7 +284,8 @@ def langevin_middle_step(state: MDState, potential, dt_fs: float, temperature: f
     """Advance one step; returns a new state sharing the RNG stream (md.py:114-145).
     ``potential`` is a ``TensorNet`` (or a ``ComposedPotential`` wrapping one, without priors)."""
     model = network_of(potential)
-    integ = DeviceIntegrator(model, state.system, state.velocities, state.masses, temperature, state.seed)
+    integ = DeviceIntegrator(model, state.system, state.velocities, state.masses, temperature, state.seed,
+                             max_num_neighbors=max_num_neighbors)
     _, c2 = ou_coefficients(dt_fs, gamma_per_ps)
     noise = state.rng.standard_normal((state.masses.size, 3)) if c2 > 0.0 else None
     integ.step_with_noise(dt_fs, gamma_per_ps, noise)
@@ -295,7 +325,8 @@ def run_simulation(state: MDState, potential, steps: int, dt_fs: float, temperat
     torch = _lib.require_cuda()
     trajectory = Trajectory(stride=stride, dt_fs=dt_fs, temperature_k=temperature,
                             gamma_per_ps=gamma_per_ps, seed=state.seed, species=state.system.species)
-    integ = DeviceIntegrator(model, state.system, state.velocities, state.masses, temperature, state.seed)
+    integ = DeviceIntegrator(model, state.system, state.velocities, state.masses, temperature, state.seed,
+                             max_num_neighbors=max_num_neighbors)
 
     def capture():
         trajectory.frames.append(integ.positions())
@@ -304,12 +335,21 @@ def run_simulation(state: MDState, potential, steps: int, dt_fs: float, temperat
     capture()
     torch.cuda.synchronize(model.device)
     start = time.perf_counter()
+    from .errors import CapacityError
+
     done = 0
     while done < steps:
         chunk = min(stride - done % stride, steps - done)
         integ.run_device(chunk, dt_fs, gamma_per_ps)
+        try:
+            integ.check_finite(f"(detected by step {done + chunk})")
+        except CapacityError:
+            # the list overflowed part-way through the chunk: the state is frozen at the last good
+            # step; grow the plan like build_with_auto_capacity and take the remaining steps
+            done = integ.steps_done()
+            integ.regrow()
+            continue
         done += chunk
-        integ.check_finite(f"(detected by step {done})")
         if done % stride == 0:
             capture()
     torch.cuda.synchronize(model.device)

@@ -31,7 +31,7 @@ def device_update(x, v, masses, forces32, dt, temp, gamma, noise=None, seed=0, c
     c1, c2 = M.ou_coefficients(dt, gamma)
     rc = lib.nnp_md_langevin_middle(xd.data_ptr(), vd.data_ptr(), fd.data_ptr(), acc.data_ptr(), sg.data_ptr(),
                                     _lib.ptr(nd), ctypes.c_uint64(seed), _lib.ptr(counter), dt, c1, c2, None,
-                                    flag.data_ptr(), n, torch.cuda.current_stream().cuda_stream)
+                                    flag.data_ptr(), n, None, 0, torch.cuda.current_stream().cuda_stream)
     assert rc == 0
     torch.cuda.synchronize()
     return xd.cpu().numpy(), vd.cpu().numpy(), int(flag.item())
@@ -142,6 +142,34 @@ def test_composed_potentials_the_device_loop_cannot_integrate_are_refused():
         P.run_simulation(state, P.ComposedPotential(priors=P.PriorStack((P.ZBL(),)), cutoff=4.0), 2, 0.5, 250.0, 1.0)
     with pytest.raises(P.ValidationError, match="derivative"):
         P.run_simulation(state, P.ComposedPotential(network=model, derivative=False), 2, 0.5, 250.0, 1.0)
+
+
+def test_neighbor_overflow_mid_run_freezes_regrows_and_resumes():
+    """Atoms that start beyond the cutoff of each other and fly together: the list outgrows a plan
+    sized for one neighbour per atom part-way through a chunk.  The integrator kernel must freeze the
+    state at the last good step (no update from stale forces, noise counter not advanced), the driver
+    regrows the plan and resumes: the trajectory equals, bit for bit, the one of a roomy model."""
+    g = np.arange(3) * 4.6
+    pos = np.stack(np.meshgrid(g[:2], g[:2], g, indexing="ij"), -1).reshape(-1, 3).astype(np.float64)
+    z = np.full(len(pos), 6)
+    centre = pos.mean(0)
+    vel = -0.06 * (pos - centre) / np.linalg.norm(pos - centre, axis=1, keepdims=True)
+    kw = dict(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=20, seed=3)
+    tight, roomy = P.TensorNet(max_num_neighbors=1, **kw), P.TensorNet(**kw)
+    out = {}
+    for name, model in (("tight", tight), ("roomy", roomy)):
+        system = P.build_system(pos, z)
+        state = P.initialize_state(system, 300.0, seed=5, velocities=vel.copy())
+        traj, report = P.run_simulation(state, model, 24, 1.0, 300.0, 2.0, stride=8)
+        out[name] = (traj, report["final_state"])
+    first_capacity = 2 * len(pos) * 1
+    assert tight._last_plan.capacity > first_capacity          # it did overflow and regrow
+    a, b = out["tight"], out["roomy"]
+    assert a[0].n_frames == b[0].n_frames == 4
+    for fa, fb in zip(a[0].frames, b[0].frames):
+        assert np.array_equal(fa, fb)
+    assert np.array_equal(a[1].velocities, b[1].velocities)
+    assert a[0].energies == b[0].energies
 
 
 def test_run_simulation_frames_determinism_and_energy_conservation():

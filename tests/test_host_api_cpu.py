@@ -24,7 +24,7 @@ def test_header_symbols_are_exported():
     for name in sorted(declared):
         assert hasattr(lib, name), f"{name} declared in nnp_b200.h but not exported"
     assert set(_lib.EXPORTED_SYMBOLS) <= declared
-    assert lib.nnp_version() == 101
+    assert lib.nnp_version() == 102
 
 
 def test_ctypes_struct_layouts_match_the_library():
