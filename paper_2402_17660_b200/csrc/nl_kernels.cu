@@ -420,8 +420,6 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
     __shared__ int s_col[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_t[FILL ? NL_WARPS : 1][FILL ? NL_MAXROW : 1];
     __shared__ int s_queue[NL_WARPS][64];
-    __shared__ int s_run_start[NL_WARPS][32], s_run_pref[NL_WARPS][32];
-    __shared__ float s_run_shift[NL_WARPS][27][3];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int s = blockIdx.x * NL_WARPS + wib;
@@ -533,6 +531,7 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
             const int cell = a.cell_id[io];
             const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
             int r_start = 0, r_len = 0;
+            float sh_x = 0.0f, sh_y = 0.0f, sh_z = 0.0f;
             const float4 la = a.slpos[s];
             if (lane < 27) {
                 const int o0 = lane / 9 - 1, o1 = (lane / 3) % 3 - 1, o2 = lane % 3 - 1;
@@ -563,9 +562,9 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
                         r_len = a.cell_start[flat + 1] - r_start;
                     }
                 }
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    s_run_shift[wib][lane][c] = o0 * g.cv[0][c] + o1 * g.cv[1][c] + o2 * g.cv[2][c];
+                sh_x = o0 * g.cv[0][0] + o1 * g.cv[1][0] + o2 * g.cv[2][0];
+                sh_y = o0 * g.cv[0][1] + o1 * g.cv[1][1] + o2 * g.cv[2][1];
+                sh_z = o0 * g.cv[0][2] + o1 * g.cv[1][2] + o2 * g.cv[2][2];
             }
             int incl = r_len;
 #pragma unroll
@@ -574,28 +573,36 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
                 if (lane >= d) incl += up;
             }
             const int total = __shfl_sync(NNP_FULL_MASK, incl, 31);
-            s_run_start[wib][lane] = r_start;
-            s_run_pref[wib][lane] = lane < 27 ? incl - r_len : 0x7fffffff;   // exclusive; sentinel past the last run
-            __syncwarp();
+            // Lane r keeps run r's start, exclusive prefix and corner shift in registers; a candidate's
+            // run is found without memory: runs are contiguous stretches of the stream, so the 32
+            // candidates of an iteration span the run that holds the first of them plus the few runs
+            // that begin inside the iteration (two ballots, then one shuffle per such run).
+            const int my_pref = lane < 27 ? incl - r_len : 0x7fffffff;   // sentinel past the last run
             const float hi2w = g.hi2w, lo2w = g.lo2w;     // window widened by the screen's error bound
             const bool one_sample = a.n_samples == 1;
-            const int *pref = s_run_pref[wib];
             for (int base = 0; base < total; base += 32) {
                 const int idx = base + lane;
+                const unsigned le = __ballot_sync(NNP_FULL_MASK, my_pref <= base);
+                unsigned inside_mask = __ballot_sync(NNP_FULL_MASK, my_pref > base && my_pref <= base + 31);
+                int r = 31 - __clz(le);                                   // last run that starts at or before base
+                while (inside_mask) {
+                    const int b = __ffs(inside_mask) - 1;
+                    inside_mask &= inside_mask - 1;
+                    if (__shfl_sync(NNP_FULL_MASK, my_pref, b) <= idx) r = b;
+                }
+                const int rs = __shfl_sync(NNP_FULL_MASK, r_start, r), rp = __shfl_sync(NNP_FULL_MASK, my_pref, r);
+                const float sx = __shfl_sync(NNP_FULL_MASK, sh_x, r), sy = __shfl_sync(NNP_FULL_MASK, sh_y, r),
+                            sz = __shfl_sync(NNP_FULL_MASK, sh_z, r);
                 bool pass = false;
                 int t = 0;
                 if (idx < total) {
-                    int r = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1)
-                        if (pref[r + step] <= idx) r += step;
-                    t = s_run_start[wib][r] + (idx - pref[r]);
+                    t = rs + (idx - rp);
                     const float4 lb = a.slpos[t];
                     const int jo = __float_as_int(lb.w);
                     if ((one_sample || a.sbatch[t] == bi) && jo != io && (full || jo > io)) {
-                        const float fx = (la.x - lb.x) - s_run_shift[wib][r][0];
-                        const float fy = (la.y - lb.y) - s_run_shift[wib][r][1];
-                        const float fz = (la.z - lb.z) - s_run_shift[wib][r][2];
+                        const float fx = (la.x - lb.x) - sx;
+                        const float fy = (la.y - lb.y) - sy;
+                        const float fz = (la.z - lb.z) - sz;
                         const float d2 = fx * fx + fy * fy + fz * fz;
                         pass = d2 <= hi2w && d2 >= lo2w;
                     }
