@@ -704,6 +704,31 @@ __global__ void __launch_bounds__(128, 5) k_embed_edge_split(TnDev d)
     }
 }
 
+// one knot-cached warp per (receiver, part) over all nine components (three radial groups in registers)
+template <int C, int CPL>
+__global__ void __launch_bounds__(128, 4) k_embed_edge_knots(TnDev d)
+{
+    NNP_PDL_SYNC();
+    constexpr int NPARTS = C / (32 * CPL);
+    if (overflowed(d)) return;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int s = gw / NPARTS, part = gw - s * NPARTS;
+    if (s >= d.n) return;
+    const int cb = part * 32 * CPL + lane * CPL;
+    float acc[9][CPL];
+    embed_row_part<C, CPL, 0, 3, 0, 9>(d, s, cb, acc);
+    float nrm[CPL];
+#pragma unroll
+    for (int v = 0; v < CPL; ++v) {
+        float c9[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) c9[q] = acc[q][v];
+        nrm[v] = c9_frob(c9, c9);
+    }
+    stv<CPL>(d.n0 + (size_t)s * C + cb, nrm);
+}
+
 // One warp's share of a receiver row: components [Q0, Q0 + NQ) = radial groups [K0, K0 + NG).
 template <int C, int CPL, int K0, int NG, int Q0, int NQ>
 __device__ __forceinline__ void message_row_part(const TnDev &d, const float *__restrict__ tab,
@@ -1953,7 +1978,8 @@ static const EdgeTuning &edge_tuning()
                                  std::min(env_int("NNP_BWD_BLOCK", 128), 128), std::min(env_int("NNP_FWD_BLOCK", 64), 128), env_int("NNP_EMB_BLOCK", 128),
                                  env_int("NNP_BWD_SPLIT", 1),   // 1 = register gather, two warps per receiver (default); 2 = bulk-copy ring
                                                                 // (measured slower: 2.15 vs 1.30 ms per step); 0 = one warp per part, monomial tables
-                                 env_int("NNP_EMB_SPLIT", 2)};  // knot-cached two-warp embedding edge kernel: 1 = always, 0 = never, 2 = up to 2 048 atoms
+                                 env_int("NNP_EMB_SPLIT", 2)};  // knot-cached embedding edge kernels: 2 = two warps per receiver up to 2 048 atoms, one warp
+                                                                // beyond (default); 1 / 3 = always two / one; 0 = the round-1 kernels on monomial tables
     return t;
 }
 #define EDGE_DISPATCH(C, cpl_req, LAUNCH)                         \
@@ -2002,7 +2028,8 @@ int run_step(TnDev &d, cudaStream_t st)
     // ---- embedding
     // two knot-cached warps per receiver pay off for small systems only (measured: 22 atoms 14.2 vs
     // 21.6 us; config C 0.343 vs 0.338 ms; config D 1.01 vs 0.88 ms): NNP_EMB_SPLIT = 2 picks by size
-    if (tune.emb_split == 1 || (tune.emb_split == 2 && n <= 2048)) { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), 2)), 64, 0, st, d))); }
+    if (tune.emb_split == 3 || (tune.emb_split == 2 && n > 2048)) { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge_knots<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), 2)), 64, 0, st, d))); }
+    else if (tune.emb_split == 1 || (tune.emb_split == 2 && n <= 2048)) { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge_split<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * 2 * (C / (32 * CPL)), 2)), 64, 0, st, d))); }
     else { NNP_PROF("k_embed_edge", st); EDGE_DISPATCH(C, tune.emb, (nnp_launch((k_embed_edge<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d))); }
     { NNP_PROF("k_embed_ln", st); nnp_launch((k_embed_ln<C>), NNP_GRID(warp_blocks), 256, 0, st, d); }
     {
@@ -2110,6 +2137,7 @@ int run_step(TnDev &d, cudaStream_t st)
         { NNP_PROF("gemm_embed_proj", st); RUN((gemm_launch<PRO_NONE, EPI_STORE>(mr, 3, st))); }
         { NNP_PROF("k_embed_edge_bwd_proj", st); nnp_launch((k_embed_edge_bwd_proj), NNP_GRID(nnp_blocks(n, EMB_PROJ_WARPS)), EMB_PROJ_WARPS * 32, 0, st, d, GB, GX); }
     }
+    // (a knot-cached variant of this fallback was measured slower: 1.62 vs 1.34 ms at config D, 22.9 vs 20.9 us at A)
     { NNP_PROF("k_embed_edge_bwd", st); EDGE_DISPATCH(C, tune.embbwd, (nnp_launch((k_embed_edge_bwd<C, CPL>), NNP_GRID(nnp_blocks((int64_t)n * (C / (32 * CPL)), tune.emb_block / 32)), tune.emb_block, 0, st, d, GC))); }
     { NNP_PROF("k_forces", st); nnp_launch((k_forces), NNP_GRID(warp_blocks), 256, 0, st, d); }
     NNP_CHECK_LAUNCH("tensornet reverse");
