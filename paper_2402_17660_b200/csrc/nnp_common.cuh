@@ -48,6 +48,8 @@ extern thread_local int g_nnp_launch_count;
 // attribute against 4.50 ms without (the waiting blocks of the next kernel take SM slots from the
 // tail of the running one), 0.266 against 0.273 ms on the 22-atom config A.  The attribute is
 // therefore only set with NNP_PDL=1 in the environment; without it NNP_PDL_SYNC() is a no-op.
+// NNP_PDL=2 sets it for the streaming mix GEMM alone (its weight staging into tensor memory then
+// overlaps the previous kernel's tail): 4.380 vs 4.410 ms on config C, no change on A, D and E.
 #if defined(__CUDA_ARCH__)
 #define NNP_PDL_SYNC()                                            \
     do {                                                          \
@@ -59,6 +61,8 @@ extern thread_local int g_nnp_launch_count;
 #endif
 
 bool nnp_pdl_enabled();
+int nnp_pdl_mode();                        // 0 = never, 1 = every launch, 2 = only launches that ask for it
+extern thread_local bool t_nnp_pdl_ask;    // set by a launch site (the streaming GEMM) right before nnp_launch
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t nnp_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -73,7 +77,9 @@ static inline cudaError_t nnp_launch(void (*kernel)(KArgs...), dim3 grid, dim3 b
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = nnp_pdl_enabled() ? 1 : 0;
+    const int mode = nnp_pdl_mode();
+    cfg.numAttrs = (mode == 1 || (mode == 2 && t_nnp_pdl_ask)) ? 1 : 0;
+    t_nnp_pdl_ask = false;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

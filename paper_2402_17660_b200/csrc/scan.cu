@@ -19,6 +19,15 @@ extern "C" const char *nnp_last_error(void) { return g_last_error; }
 
 thread_local int g_nnp_launch_count = 0;
 
+thread_local bool t_nnp_pdl_ask = false;
+int nnp_pdl_mode()
+{
+    static const int mode = [] {
+        const char *v = getenv("NNP_PDL");
+        return v ? atoi(v) : 0;
+    }();
+    return mode;
+}
 bool nnp_pdl_enabled()
 {
     static const bool on = [] {

@@ -662,6 +662,7 @@ static int launch_stream(const GemmBatch &b, int count, cudaStream_t stream)
         used += c;
     }
     for (int i = count; i < 4; ++i) sc.cta_begin[i] = used;
+    t_nnp_pdl_ask = true;      // NNP_PDL=2: only this kernel starts early (its weight staging overlaps the previous kernel's tail)
     nnp_launch((gemm_stream_kernel<PRO, EPI>), NNP_GRID(used), ST_THREADS, smem, stream, b, sc);
     NNP_CHECK_LAUNCH("gemm_stream");
     return NNP_OK;
