@@ -274,6 +274,25 @@ def test_second_order_pullback_against_reference_golden(golden):
             P.distance_pullback_second(coincident, np.ones(8), np.ones((3, 3)))
 
 
+def test_config_e_triclinic_box_full_list_bit_exact():
+    """The 100 000-atom triclinic box of config E with the flags the model uses (full list, self
+    loops): pairs, deltas and distances equal the C oracle's bit for bit, and the cell-order
+    numbering of the model path (NNP_NL_RENUMBER) holds the same rows after mapping back."""
+    z, pos, batch, box = synth.config_e_triclinic()
+    n = len(pos)
+    system = make_system(pos, batch, box)
+    spec = P.NeighborSpec(cutoff_upper=5.0, capacity=64 * n, strategy="cell", full_list=True,
+                          include_self_loops=True)
+    nl = P.build_neighbor_list(system, spec)
+    ref = O.build_neighbor_list(pos, batch, box, 5.0, 64 * n, strategy="cell", full_list=True,
+                                include_self_loops=True)
+    c = ref.count
+    assert nl.count == c
+    assert np.array_equal(nl.pairs[:c].cpu().numpy(), ref.pairs[:c])
+    assert np.array_equal(nl.deltas[:c].cpu().numpy(), ref.deltas[:c])
+    assert np.array_equal(nl.distances[:c].cpu().numpy(), ref.distances[:c])
+
+
 def test_one_million_atoms_bit_exact():
     """1 048 576 atoms (the largest point of config B's sweep): pairs, deltas and distances of the
     half list equal the C oracle's bit for bit (the oracle needs a few seconds on one core)."""
