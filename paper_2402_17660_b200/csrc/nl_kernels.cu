@@ -39,6 +39,7 @@ struct GridDev {
     // (back substitution through the lower-triangular cell vectors), the cell's perpendicular widths,
     // and whether the three widths are orthogonal (then the gaps to a neighbour cell add in quadrature)
     float wid[3];
+    float icv[3];      // 1 / cv[k][k]
     float cull2;       // squared reach beyond which a whole neighbour cell cannot hold a pair (widened)
     int ortho;
 };
@@ -71,6 +72,8 @@ struct NlArgs {
     int *sample_ptr, *scratch_col, *scratch_t, *stage_t;
     double *spos;
     float4 *slpos;   // cell strategy: (position relative to the atom's own cell corner, original index)
+    int4 *scell;     // cell strategy: grid coordinates of the sorted atom's cell (and the flat index): the row
+                     // scan needs them per atom and a division by a runtime grid size costs ~25 instructions
     double *bounds_partial;
     GridDev *grid;
     // outputs
@@ -230,6 +233,9 @@ __global__ void k_grid_setup(NlArgs a, int n_partial)
         g.wid[0] = (float)(1.0 / sqrt(g0[0] * g0[0] + g0[1] * g0[1] + g0[2] * g0[2]));
         g.wid[1] = (float)(1.0 / sqrt(g1[1] * g1[1] + g1[2] * g1[2]));
         g.wid[2] = (float)c22;
+        g.icv[0] = (float)(1.0 / c00);
+        g.icv[1] = (float)(1.0 / c11);
+        g.icv[2] = (float)(1.0 / c22);
         g.ortho = (c10 == 0.0 && c20 == 0.0 && c21 == 0.0) ? 1 : 0;
         // a cell is skipped when even its nearest plane is farther than the cutoff plus 0.1 % of a
         // cell (three orders above the float32 error of the local coordinates)
@@ -306,6 +312,7 @@ __global__ void k_cell_rank(NlArgs a)
     const GridDev g = *a.grid;
     const double x = a.pos[3 * (size_t)i], y = a.pos[3 * (size_t)i + 1], z = a.pos[3 * (size_t)i + 2];
     const int cc[3] = {c / (g.dims[1] * g.dims[2]), (c / g.dims[2]) % g.dims[1], c % g.dims[2]};
+    a.scell[s] = make_int4(cc[0], cc[1], cc[2], c);
     double lx, ly, lz;
     if (a.periodic) {
         double w[3];
@@ -528,14 +535,14 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
             // needed); every iteration then screens 32 consecutive candidates of the concatenated
             // runs, whatever cell boundaries fall between them.
             const GridDev g = *a.grid;
-            const int cell = a.cell_id[io];
+            const int4 cc = a.scell[s];
             const int m0 = g.dims[0], m1 = g.dims[1], m2 = g.dims[2];
             int r_start = 0, r_len = 0;
             float sh_x = 0.0f, sh_y = 0.0f, sh_z = 0.0f;
             const float4 la = a.slpos[s];
             if (lane < 27) {
                 const int o0 = lane / 9 - 1, o1 = (lane / 3) % 3 - 1, o2 = lane % 3 - 1;
-                int n0 = cell / (m1 * m2) + o0, n1 = (cell / m2) % m1 + o1, n2 = cell % m2 + o2;
+                int n0 = cc.x + o0, n1 = cc.y + o1, n2 = cc.z + o2;
                 bool inside = true;
                 if (a.periodic) {
                     n0 = n0 < 0 ? n0 + m0 : (n0 >= m0 ? n0 - m0 : n0);
@@ -548,9 +555,9 @@ __global__ void __launch_bounds__(NL_THREADS, FILL ? 6 : 0) k_rows(NlArgs a)
                     // Cull cells that lie wholly beyond the cutoff of THIS atom: the neighbour cell in
                     // direction o along axis k starts at a plane whose perpendicular distance is
                     // (1 - f_k) w_k (o = +1) or f_k w_k (o = -1), f = fractional position in the own cell.
-                    const float f2 = la.z / g.cv[2][2];
-                    const float f1 = (la.y - f2 * g.cv[2][1]) / g.cv[1][1];
-                    const float f0 = (la.x - f1 * g.cv[1][0] - f2 * g.cv[2][0]) / g.cv[0][0];
+                    const float f2 = la.z * g.icv[2];
+                    const float f1 = (la.y - f2 * g.cv[2][1]) * g.icv[1];
+                    const float f0 = (la.x - f1 * g.cv[1][0] - f2 * g.cv[2][0]) * g.icv[0];
                     const float gap0 = o0 == 0 ? 0.0f : fmaxf(o0 > 0 ? 1.0f - f0 : f0, 0.0f) * g.wid[0];
                     const float gap1 = o1 == 0 ? 0.0f : fmaxf(o1 > 0 ? 1.0f - f1 : f1, 0.0f) * g.wid[1];
                     const float gap2 = o2 == 0 ? 0.0f : fmaxf(o2 > 0 ? 1.0f - f2 : f2, 0.0f) * g.wid[2];
@@ -761,6 +768,7 @@ size_t carve(NlArgs &a, const nnp_nl_params *p, void *ws)
     a.stage_t = ar.take<int>(n * (size_t)a.stage_w);
     a.spos = ar.take<double>(3 * n);
     a.slpos = ar.take<float4>(n);
+    a.scell = ar.take<int4>(n);
     a.bounds_partial = ar.take<double>(6 * BOUNDS_BLOCKS);
     a.grid = ar.take<GridDev>(1);
     return ar.bytes();

@@ -276,8 +276,7 @@ def test_second_order_pullback_against_reference_golden(golden):
 
 def test_config_e_triclinic_box_full_list_bit_exact():
     """The 100 000-atom triclinic box of config E with the flags the model uses (full list, self
-    loops): pairs, deltas and distances equal the C oracle's bit for bit, and the cell-order
-    numbering of the model path (NNP_NL_RENUMBER) holds the same rows after mapping back."""
+    loops): pairs, deltas and distances equal the C oracle's bit for bit."""
     z, pos, batch, box = synth.config_e_triclinic()
     n = len(pos)
     system = make_system(pos, batch, box)
