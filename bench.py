@@ -319,10 +319,18 @@ def main():
     sharded = world > 1 and args.workload == "D"
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    # NNP_BENCH_SHARE_GPU=1 (functional test of the multi-rank path on a one-GPU box): every rank
+    # uses cuda:0 and the gather runs over gloo, since NCCL refuses two ranks on one device
+    share_gpu = os.environ.get("NNP_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2402_17660_b200 as P
     from paper_2402_17660_b200 import _lib
