@@ -185,7 +185,8 @@ class _Plan:
     """Everything that is fixed for one input shape: buffers, neighbor engine, graph."""
 
     __slots__ = ("key", "n", "n_samples", "capacity", "engine", "workspace", "z", "batch", "pos32",
-                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box", "batch_is_zero", "proj")
+                 "pos64", "energy", "forces", "per_atom", "graph", "notes", "box", "batch_is_zero", "proj",
+                 "io")
 
 
 class TensorNet:
@@ -405,6 +406,7 @@ class TensorNet:
         plan.forces = torch.zeros((n, 3), dtype=torch.float32, device=dev)
         plan.per_atom = torch.zeros(n, dtype=torch.float32, device=dev)
         plan.graph = None
+        plan.io = None
         self._plans[key] = plan
         return plan
 
@@ -512,6 +514,107 @@ class TensorNet:
 
     __call__ = forward
 
+    # ------------------------------------------------- host in, host out: one graph, one synchronisation
+    def _host_io(self, plan: _Plan, with_batch: bool):
+        """Pinned staging buffers of a plan and ONE captured graph that copies the inputs up, runs the
+        whole step and copies energies, forces, per-atom energies and the overflow counter down."""
+        torch = self._torch
+        io = plan.io
+        if io is not None and io["with_batch"] == with_batch:
+            return io
+        pos_dev = plan.pos32 if plan.pos32 is not None else plan.pos64
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype).pin_memory()
+        io = {"with_batch": with_batch, "z": pin(plan.z), "batch": pin(plan.batch), "pos": pin(pos_dev),
+              "energy": pin(plan.energy), "forces": pin(plan.forces), "per_atom": pin(plan.per_atom),
+              "counts": pin(plan.engine.counts)}
+
+        def enqueue():
+            plan.z.copy_(io["z"], non_blocking=True)
+            if with_batch:
+                plan.batch.copy_(io["batch"], non_blocking=True)
+            pos_dev.copy_(io["pos"], non_blocking=True)
+            self._enqueue(plan)
+            io["energy"].copy_(plan.energy, non_blocking=True)
+            io["forces"].copy_(plan.forces, non_blocking=True)
+            io["per_atom"].copy_(plan.per_atom, non_blocking=True)
+            io["counts"].copy_(plan.engine.counts, non_blocking=True)
+
+        io["z"].zero_()
+        io["batch"].zero_()
+        io["pos"].copy_(pos_dev)                 # a valid configuration for the warm-up run
+        io["z"].copy_(plan.z)
+        io["batch"].copy_(plan.batch)
+        if self.use_graph:
+            enqueue()
+            torch.cuda.synchronize(self.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                enqueue()
+            io["run"] = graph.replay
+        else:
+            io["run"] = enqueue
+        plan.io = io
+        return io
+
+    def forward_host(self, z, pos, batch=None, box=None, *, n_samples: Optional[int] = None,
+                     check: bool = True, copy: bool = True):
+        """``forward`` for callers whose data lives on the host (the reference's own call shape:
+        numpy in, numpy out): returns ``(energy [n_samples], forces [N, 3])`` as numpy float32 arrays.
+
+        The inputs are written into pinned staging buffers and ONE captured graph does the rest
+        (host-to-device copies, neighbor search, forward and force sweep, device-to-host copies of
+        the results and of the overflow counter), followed by one stream synchronisation - instead
+        of two copies up, a graph, a synchronising counter read and two copies down.
+        ``copy=False`` returns views of the pinned result buffers (valid until the next call)."""
+        torch = self._torch
+        pos_t = torch.as_tensor(np.array(pos) if isinstance(pos, np.ndarray) and not pos.flags.writeable else pos)
+        z_t = torch.as_tensor(np.array(z) if isinstance(z, np.ndarray) and not z.flags.writeable else z)
+        if pos_t.is_cuda or z_t.is_cuda:
+            raise ValidationError("forward_host takes host arrays; use forward() for device tensors")
+        if pos_t.dim() != 2 or pos_t.shape[1] != 3:
+            raise ValidationError("positions must have shape (N, 3)")
+        n = pos_t.shape[0]
+        if z_t.shape != (n,):
+            raise ValidationError(f"length mismatch: {n} positions but {tuple(z_t.shape)} species")
+        if pos_t.dtype not in (torch.float32, torch.float64):
+            pos_t = pos_t.to(torch.float32)
+        batch_t = None if batch is None else torch.as_tensor(batch)
+        if batch_t is None:
+            n_samples = 1
+        else:
+            if batch_t.shape != (n,):
+                raise ValidationError(f"length mismatch: {n} positions but {tuple(batch_t.shape)} batch codes")
+            if n_samples is None:
+                n_samples = int(batch_t[-1]) + 1
+            if check:
+                self._batch_checked(batch_t, n, n_samples, remember=isinstance(batch, torch.Tensor))
+        box_obj = self._as_box(box)
+        proj = self._species_checked(z_t, n, check, remember=isinstance(z, torch.Tensor))
+        capacity = self._capacity_hint.get((n, n_samples), self.neighbor_capacity(n))
+        plan = self._plan(n, n_samples, box_obj, capacity, pos_t.dtype == torch.float32, proj)
+        if plan.graph is None and self.use_graph:
+            # first use of this shape: the ordinary path creates (and, on overflow, regrows) the plan
+            self.forward(z_t, pos_t, batch_t, box_obj, n_samples=n_samples, check=True, clone=False)
+            plan = self._last_plan
+        self._last_plan = plan
+        io = self._host_io(plan, batch_t is not None)
+        io["z"].copy_(z_t)
+        if batch_t is not None:
+            io["batch"].copy_(batch_t)
+            plan.batch_is_zero = False
+        elif not plan.batch_is_zero:
+            plan.batch.zero_()
+            plan.batch_is_zero = True
+        io["pos"].copy_(pos_t)
+        io["run"]()
+        torch.cuda.current_stream().synchronize()
+        if check and int(io["counts"][0]) > plan.capacity:
+            # overflow: let forward() grow the capacity (it re-runs the step), then answer from the new plan
+            self.forward(z_t, pos_t, batch_t, box_obj, n_samples=n_samples, check=True, clone=False)
+            return self.forward_host(z, pos, batch, box, n_samples=n_samples, check=check, copy=copy)
+        e, f = io["energy"].numpy(), io["forces"].numpy()
+        return (e.copy(), f.copy()) if copy else (e, f)
+
     # ---------------------------------------------------------- resident replay (benchmarks, MD)
     def prepare(self, z, pos, batch=None, box=None, *, n_samples: Optional[int] = None):
         """Run one checked step and return the plan, whose inputs now live in HBM and whose
@@ -550,11 +653,10 @@ class TensorNet:
                 f"species code {int(system.species.max())} is out of range for "
                 f"max_z={self.config.max_z}")
         if neighbors is None:
-            e, f = self.forward(system.species, system.positions, system.batch, system.box,
-                                n_samples=system.n_samples)
-            plan = self._last_plan
-            return EnergyForces(e.cpu().numpy(), f.cpu().numpy() if forces else None,
-                                plan.per_atom.cpu().numpy())
+            e, f = self.forward_host(system.species, system.positions, system.batch, system.box,
+                                     n_samples=system.n_samples)
+            per_atom = self._last_plan.io["per_atom"].numpy().copy()
+            return EnergyForces(e, f if forces else None, per_atom)
         spec = neighbors.spec
         if not spec.full_list:
             raise ValidationError(

@@ -504,3 +504,36 @@ def test_embed_projection_is_chosen_by_size_and_species():
     assert not small._use_projection(z, 5000)
     with pytest.raises(P.ValidationError):
         P.TensorNet(embedding_dimension=64, num_layers=1, num_rbf=32, embed_projection=True)
+
+
+def test_forward_host_equals_forward_and_regrows(rng):
+    """forward_host (numpy in, numpy out, one graph with the copies inside, one synchronisation) returns
+    exactly what forward returns, with and without batch codes, for float32 and float64 positions, when
+    the inputs change between calls, and after a capacity overflow."""
+    z, pos, batch, _ = small_open(rng, 36)
+    model = P.TensorNet(embedding_dimension=32, num_layers=2, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)
+    for dtype in (np.float32, np.float64):
+        p = pos.astype(dtype)
+        for b in (batch, None):
+            e, f = model(torch.as_tensor(z), torch.as_tensor(p), None if b is None else torch.as_tensor(b))
+            eh, fh = model.forward_host(z, p, b)
+            assert eh.dtype == np.float32 and fh.shape == (len(z), 3)
+            assert np.array_equal(eh, e.cpu().numpy()) and np.array_equal(fh, f.cpu().numpy())
+            p2 = (p + rng.normal(0, 0.05, p.shape)).astype(dtype)          # same shape, new numbers: graph replay
+            e2, f2 = model(torch.as_tensor(z), torch.as_tensor(p2), None if b is None else torch.as_tensor(b))
+            eh2, fh2 = model.forward_host(z, p2, b, copy=False)
+            assert np.array_equal(eh2, e2.cpu().numpy()) and np.array_equal(fh2, f2.cpu().numpy())
+    tight = P.TensorNet(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1,
+                        max_num_neighbors=1)
+    sparse = (np.arange(36)[:, None] * np.array([4.5, 0.0, 0.0])).astype(np.float32)
+    tight.forward_host(z, sparse)                                             # fits: self loops only
+    eh, fh = tight.forward_host(z, pos.astype(np.float32))                    # overflows, regrows, answers
+    e, f = model.__class__(embedding_dimension=32, num_layers=1, num_rbf=8, cutoff_upper=4.0, max_z=10, seed=1)(
+        torch.as_tensor(z), torch.as_tensor(pos, dtype=torch.float32))
+    assert np.array_equal(eh, e.cpu().numpy()) and np.array_equal(fh, f.cpu().numpy())
+    with pytest.raises(P.ValidationError, match="host arrays"):
+        model.forward_host(torch.as_tensor(z).cuda(), torch.as_tensor(pos).cuda())
+    res = model.evaluate(P.build_system(pos, z, batch=batch))
+    e, f = model(torch.as_tensor(z), torch.as_tensor(pos), torch.as_tensor(batch))
+    assert np.array_equal(res.energy, e.cpu().numpy()) and np.array_equal(res.forces, f.cpu().numpy())
+    assert np.allclose(np.bincount(batch, weights=res.per_atom_energy), res.energy, rtol=1e-5)
