@@ -434,7 +434,9 @@ def main():
     for _ in range(3):
         e2e_step()
     barrier()
-    e2e_steps = max(10, args.steps // 2)
+    # sub-millisecond steps: enough iterations for ~60 ms of timed work, so that one host hiccup
+    # does not decide the number (15 steps of the 22-atom config are a 5 ms window)
+    e2e_steps = max(10, args.steps // 2, min(400, int(60.0 / max(ms_per_step, 1e-3))))
     start.record()
     for _ in range(e2e_steps):
         e2e_step()
