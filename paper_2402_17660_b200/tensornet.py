@@ -475,7 +475,7 @@ class TensorNet:
         if batch is None:
             batch_t, n_samples = None, 1
         else:
-            batch_t = torch.as_tensor(batch)
+            batch_t = torch.as_tensor(np.array(batch) if isinstance(batch, np.ndarray) and not batch.flags.writeable else batch)
             if batch_t.shape != (n,):
                 raise ValidationError(f"length mismatch: {n} positions but {tuple(batch_t.shape)} batch codes")
             if n_samples is None:
@@ -578,7 +578,8 @@ class TensorNet:
             raise ValidationError(f"length mismatch: {n} positions but {tuple(z_t.shape)} species")
         if pos_t.dtype not in (torch.float32, torch.float64):
             pos_t = pos_t.to(torch.float32)
-        batch_t = None if batch is None else torch.as_tensor(batch)
+        batch_t = None if batch is None else torch.as_tensor(
+            np.array(batch) if isinstance(batch, np.ndarray) and not batch.flags.writeable else batch)
         if batch_t is None:
             n_samples = 1
         else:
